@@ -1,0 +1,204 @@
+"""Generate golden fixtures by running the UNMODIFIED reference (vpflow) in this container.
+
+Test infrastructure only. This script imports the reference package from
+/root/reference/pkg/src (read-only) and records, per BASELINE config, the
+outputs of the canonical per-step loop (reference has no
+driver, the loop follows SPEC.md:465-468):
+
+    r = density.compute_rho(ctx, n)                  # density.py:72-91
+    phi, spec = poisson.solve_poisson(r.density)     # poisson.py:90-112
+    fit = spline.fit_spline(phi, grid)               # spline.py:71-86
+    hist.append(fit)                                 # spline.py:132-142
+    W = poisson.electric_energy(spec)                # poisson.py:115-120
+    E = kernels.eval_E_many(fit.coeffs, L, x_node_matrix(grid))   # kernels.py:102-123
+
+It also records trace goldens: seeded random (x, v) pushed through a real
+history by kernels.trace_backward (kernels.py:390-412, numba backend) with
+half_kick 0 and 1.
+
+The fixtures are committed under tests/golden/*.npz; the GPU box never runs
+this script (/root/reference does not exist there).
+
+Usage:  python tests/golden/make_golden.py wl1 ts1 ...   (default: all)
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import os
+import platform
+import sys
+import time
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+# Config table: SURVEY.md §8(d) / BASELINE.json configs. "keep" = number of
+# steps (0..keep-1) whose rho/coeffs/E are stored; W and stats are stored for
+# every step that was run.
+CONFIGS = {
+    # BASELINE configs
+    "wl1": dict(d=1, Nx=64, Nv=256, vmax=6.0, tau=1 / 8, N=240, bench="weak_landau_1d", alpha=None, keep=51),
+    "ts1": dict(d=1, Nx=64, Nv=512, vmax=10.0, tau=1 / 16, N=1600, bench="two_stream_1d", alpha=None, keep=51),
+    "sl1": dict(d=1, Nx=256, Nv=2048, vmax=8.0, tau=1 / 16, N=800, bench="weak_landau_1d", alpha=0.5, keep=51),
+    "wl2": dict(d=2, Nx=32, Nv=64, vmax=6.0, tau=1 / 8, N=160, bench="strong_landau_2d", alpha=0.01, keep=51),
+    "wl3": dict(d=3, Nx=16, Nv=32, vmax=6.0, tau=1 / 8, N=10, bench="weak_landau_3d", alpha=0.01, keep=11),
+    # reduced / small cases (fast parity cases; oracle finishes in seconds)
+    "wl3r": dict(d=3, Nx=16, Nv=8, vmax=6.0, tau=1 / 8, N=80, bench="weak_landau_3d", alpha=0.01, keep=81),
+    "kat_wl": dict(d=1, Nx=32, Nv=128, vmax=10.0, tau=1 / 16, N=160, bench="weak_landau_1d", alpha=None, keep=161),
+    "tiny2": dict(d=2, Nx=8, Nv=8, vmax=6.0, tau=1 / 8, N=24, bench="strong_landau_2d", alpha=0.5, keep=25),
+    "tiny3": dict(d=3, Nx=8, Nv=4, vmax=6.0, tau=1 / 8, N=12, bench="two_stream_3d", alpha=None, keep=13),
+    "eq1": dict(d=1, Nx=32, Nv=128, vmax=10.0, tau=1 / 16, N=160, bench="weak_landau_1d", alpha=0.0, keep=1),
+}
+
+
+# history length used for the trace goldens
+TRACE_N = {"kat_wl": 40, "tiny2": 20, "tiny3": 12, "wl3r": 16}
+
+
+def build(cfg):
+    from vpflow.grids import GridSpec
+    from vpflow.initial import InitialCondition, VelocityProfile, make_benchmark
+
+    d = cfg["d"]
+    if cfg["bench"] == "two_stream_3d":
+        # 3-d two-stream needs L = 10*pi (initial.py:115); smaller grid here
+        L = 10.0 * math.pi
+        ic = make_benchmark("two_stream_3d")
+    else:
+        L = 4.0 * math.pi
+        if cfg["bench"] == "weak_landau_3d":
+            # not a reference built-in; SURVEY.md §0 fact 10 / §8(d)
+            ic = InitialCondition(benchmark="weak_landau_3d", d=3, L=L, alpha=cfg["alpha"], k=0.5,
+                                  profiles=(VelocityProfile(),) * 3)
+        elif cfg["alpha"] is not None:
+            ic = make_benchmark(cfg["bench"], alpha=cfg["alpha"])
+        else:
+            ic = make_benchmark(cfg["bench"])
+    g = GridSpec(d=d, L=L, Nx=cfg["Nx"], Nv=cfg["Nv"], vmax=cfg["vmax"])
+    return g, ic
+
+
+def ic_descriptor(ic):
+    return dict(benchmark=ic.benchmark, d=ic.d, L=ic.L, alpha=ic.alpha, k=ic.k,
+                profiles=[dict(centers=list(p.centers), weights=list(p.weights), power=p.power)
+                          for p in ic.profiles])
+
+
+def run(name, cfg):
+    from vpflow import density, kernels, poisson, spline
+    from vpflow.flow import FlowContext
+    from vpflow.grids import x_node_matrix
+
+    g, ic = build(cfg)
+    tau = cfg["tau"]
+    N = cfg["N"]
+    keep = cfg["keep"]
+    hist = spline.PotentialHistory(g, tau)
+    ctx = FlowContext(history=hist, ic=ic, tau=tau, grid=g)
+    Xn = x_node_matrix(g)
+    nodes = g.n_nodes
+    rho = np.zeros((keep, nodes))
+    coeffs = np.zeros((keep, nodes))
+    E = np.zeros((keep, nodes, g.d))
+    W = np.zeros(N + 1)
+    stats = np.zeros((N + 1, 3))
+    t_rho = np.zeros(N + 1)
+    t_tail = np.zeros(N + 1)
+    evals = []
+    t0 = time.time()
+    for n in range(N + 1):
+        a = time.perf_counter()
+        r = density.compute_rho(ctx, n)
+        b = time.perf_counter()
+        phi, spec = poisson.solve_poisson(r.density)
+        fit = spline.fit_spline(phi, g)
+        hist.append(fit)
+        W[n] = poisson.electric_energy(spec)
+        c = time.perf_counter()
+        t_rho[n] = b - a
+        t_tail[n] = c - b
+        stats[n] = (r.neutralization, r.f_min, r.f_max)
+        evals.append(ctx.field_evals)
+        if n < keep:
+            rho[n] = r.density.values.reshape(-1)
+            coeffs[n] = np.asarray(fit.coeffs).reshape(-1)
+            E[n] = kernels.eval_E_many(fit.coeffs, g.L, Xn)
+        if n % 50 == 0:
+            print(f"[{name}] step {n}/{N}  W={W[n]:.6e}  t={time.time() - t0:.1f}s", flush=True)
+    np.savez_compressed(
+        os.path.join(OUT, f"{name}.npz"),
+        rho=rho, coeffs=coeffs, E=E, W=W, stats=stats, t_rho=t_rho, t_tail=t_tail,
+        field_evals=np.array(evals, dtype=np.int64), rho_bar=np.array(ctx.rho_bar),
+    )
+    meta = dict(name=name, cfg=cfg, L=g.L, ic=ic_descriptor(ic), rho_bar=ctx.rho_bar,
+                wall_s=time.time() - t0, rho_s=float(t_rho.sum()), tail_s=float(t_tail.sum()),
+                field_evals=int(ctx.field_evals), host=host_info())
+    with open(os.path.join(OUT, f"{name}.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+    print(f"[{name}] done in {time.time() - t0:.1f}s", flush=True)
+    return g, ic, hist
+
+
+def trace_goldens(name, g, stack, tau, n, M=2000, seed=1234):
+    """Seeded points through a stored history (stack: (rows, Nx, ..)) with both half_kick values."""
+    from vpflow import kernels
+
+    rng = np.random.default_rng(seed)
+    d = g.d
+    X0 = rng.uniform(0.0, g.L, size=(M, d))
+    V0 = rng.uniform(-g.vmax, g.vmax, size=(M, d))
+    stack = np.ascontiguousarray(stack)
+    out = {"Xin": X0, "Vin": V0, "coeffs": stack[: n + 1].reshape(n + 1, -1), "n": np.array(n)}
+    for hk in (0, 1):
+        X = X0.copy()
+        V = V0.copy()
+        ev = kernels.trace_backward(stack[: n + 1] if hk else stack[:n], g.L, n, tau, X, V, bool(hk))
+        out[f"X{hk}"] = X
+        out[f"V{hk}"] = V
+        out[f"evals{hk}"] = np.array(ev)
+    # numpy twin on the same inputs (reference's in-tree second backend)
+    kernels.set_backend("numpy")
+    for hk in (0, 1):
+        X = X0.copy()
+        V = V0.copy()
+        kernels.trace_backward(stack[: n + 1] if hk else stack[:n], g.L, n, tau, X, V, bool(hk))
+        out[f"Xnp{hk}"] = X
+        out[f"Vnp{hk}"] = V
+    kernels.set_backend("numba")
+    np.savez_compressed(os.path.join(OUT, f"trace_{name}.npz"), L=np.array(g.L), tau=np.array(tau), **out)
+
+
+def host_info():
+    try:
+        cpu = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
+    except Exception:  # pragma: no cover
+        cpu = platform.processor()
+    import numba
+
+    return dict(cpu=cpu, cores=os.cpu_count(), numba_threads=numba.config.NUMBA_NUM_THREADS,
+                numpy=np.__version__, numba=numba.__version__, python=platform.python_version())
+
+
+def main(argv):
+    sys.path.insert(0, REF)
+    names = argv or list(CONFIGS)
+    for name in names:
+        if name.startswith("trace_"):
+            # trace goldens only, from the coefficients stored by an earlier run
+            base = name[len("trace_"):]
+            g, _ = build(CONFIGS[base])
+            z = np.load(os.path.join(OUT, f"{base}.npz"))
+            stack = z["coeffs"].reshape((-1,) + (g.Nx,) * g.d)
+            trace_goldens(base, g, stack, CONFIGS[base]["tau"], TRACE_N[base])
+            continue
+        g, ic, hist = run(name, CONFIGS[name])
+        if name in TRACE_N:
+            trace_goldens(name, g, hist.stacked(), CONFIGS[name]["tau"], TRACE_N[name])
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])
