@@ -1,0 +1,322 @@
+"""bench.py -- backtraced point-steps/s (FP64) and wall time to t_end (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config ts1|wl1|sl1|wl2|wl3] [--impl reference]
+
+A bench "step" is ONE FULL RUN of the configured workload to t_end (ts1: the
+n = 0..1600 loop, P * N(N+1)/2 = 4.197e10 point-steps), all time steps on the
+GPU: trace + f0 + v-reduction kernel, fixed-order block combine, single-CTA
+Poisson / spline / append / energy kernel.  `value` = point-steps / device time
+of the run (CUDA events on the library stream, outputs left in HBM; L2 flushed
+between runs); `ms_per_step` = wall time to t_end of one run.  `e2e` = the same
+metric through the public API call a user makes (Simulation(...).run() with
+host numpy outputs: per-step rho / E / W / stats copied device -> host inside
+the timed region).  N > 1 ranks (torchrun): velocity-block sharding with one
+NCCL allreduce per step (paper_2301_05581_b200/dist.py), device time = max
+over ranks.
+
+`--impl reference`: the reference's CPU path restated by the oracle (C trace,
+all host threads, + numpy, cpu_baseline.kind = "port"; the reference itself is
+Python + numba and cannot travel to the GPU box) on a bounded sample of the
+same workload; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="ts1")
+    ap.add_argument("--impl", default="nufi", choices=["nufi", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU sample length")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._loop, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 8:
+                for nm, v in zip(names, r[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port on a bounded sample of the workload
+# ---------------------------------------------------------------------------
+
+def cpu_sample(name: str, seconds: float):
+    """Run the oracle loop n = 0, 1, ... until `seconds` elapse (or t_end); returns the rate."""
+    from oracle import oracle as O
+    from paper_2301_05581_b200.configs import workload
+
+    w = workload(name)
+    c = O.case(name)
+    threads = O.max_threads()
+    run = O.OracleRun(c, threads=threads)
+    run.step(0)  # warm-up (not timed)
+    run.step(1)
+    t0 = time.perf_counter()
+    n = 2
+    while n <= w.n_steps:
+        run.step(n)
+        n += 1
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = time.perf_counter() - t0
+    ps = c.n_nodes * c.n_cells * (sum(range(2, n)))
+    return {"value": ps / dt, "unit": "point-steps/s", "cores": threads, "kind": "port",
+            "sample": f"{name} steps 2..{n - 1} of {w.n_steps} (whole loop: trace + f0 + reduce + Poisson/spline), "
+                      f"{ps:.3e} point-steps in {dt:.1f} s; oracle C trace (OpenMP) + numpy",
+            "seconds": dt}
+
+
+def reference_arm(args, rank: int):
+    from paper_2301_05581_b200.configs import workload
+
+    if rank != 0:
+        return
+    w = workload(args.config)
+    per = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_sample(args.config, per / 4)
+    vals = []
+    last = None
+    for _ in range(args.steps):
+        last = cpu_sample(args.config, per)
+        vals.append(last["value"])
+    v = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": "backtraced point-steps/s (FP64)", "value": v, "unit": "point-steps/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * w.point_steps / v, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic BASELINE config, no dataset)",
+        "config": {"workload": args.config, "description": w.description, "point_steps_per_run": w.point_steps},
+        "cpu_baseline": {"value": v, "unit": "point-steps/s", "cores": last["cores"], "kind": "port",
+                         "sample": last["sample"]},
+        "e2e": {"value": v, "unit": "point-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "ms_per_step extrapolates the sampled rate to the full run to t_end",
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def flush_l2(torch, buf):
+    buf.add_(1.0)  # 256 MiB write > 126 MB L2
+
+
+def gpu_arm(args, rank: int, world: int):
+    import ctypes
+
+    import torch
+
+    import paper_2301_05581_b200 as nufi
+    from paper_2301_05581_b200 import _lib
+    from paper_2301_05581_b200.configs import ALGO_FLOPS, workload
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    w = workload(args.config)
+    g = w.grid
+    N = w.n_steps
+    steps_per_run = N + 1
+    lib = _lib.load()
+    flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    if world > 1:
+        import torch.distributed as dist
+
+        from paper_2301_05581_b200.dist import DistributedSimulation
+
+        sim = DistributedSimulation(g, w.ic, w.tau, N)
+    else:
+        sim = nufi.Simulation(g, w.ic, w.tau, N, device=dev, stream=stream.cuda_stream)
+    dev_out = dict(rho=torch.empty((steps_per_run, g.n_nodes), dtype=torch.float64, device="cuda"),
+                   E=torch.empty((steps_per_run, g.n_nodes, g.d), dtype=torch.float64, device="cuda"),
+                   W=torch.empty(steps_per_run, dtype=torch.float64, device="cuda"),
+                   stats=torch.empty((steps_per_run, 3), dtype=torch.float64, device="cuda"))
+
+    def one_run():
+        sim.history.truncate(0)
+        sim.run(outputs=dev_out)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        one_run()
+    torch.cuda.synchronize()
+
+    # ---- timed runs: device time per run, L2 flushed between runs ----
+    times = []
+    wall = []
+    with ClockSampler(dev) as clocks:
+        for _ in range(args.steps):
+            flush_l2(torch, flush)
+            barrier()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            e0.record(stream)
+            one_run()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            wall.append(time.perf_counter() - t0)
+            times.append(e0.elapsed_time(e1) / 1e3)
+    t_dev = float(np.sum(times))
+    if world > 1:
+        tt = torch.tensor([t_dev], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_dev = float(tt.item())
+    ps_run = w.point_steps
+    value = args.steps * ps_run / t_dev
+    ms_per_run = 1e3 * t_dev / args.steps
+
+    # ---- e2e: the public API with host outputs (per-step D2H inside the timed region) ----
+    e2e_times = []
+    d2h = steps_per_run * (g.n_nodes * (1 + g.d) + 4) * 8
+    if world == 1:
+        for i in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = nufi.Simulation(g, w.ic, w.tau, N, device=dev).run()
+            _ = float(res.W[-1])  # host-side read of the result
+            if i >= args.warmup:
+                e2e_times.append(time.perf_counter() - t0)
+        e2e_value = args.steps * ps_run / float(np.sum(e2e_times))
+    else:
+        e2e_value = None
+
+    # ---- roofline: one additional identical run with per-launch CUDA events ----
+    h = sim.history.handle
+    lib.nufi_profiling(h.h, 1)
+    one_run()
+    prof = np.zeros(8)
+    lib.nufi_profiling_read(h.h, prof.ctypes.data)
+    lib.nufi_profiling(h.h, 0)
+    trace_ms, trace_launches, reduce_ms, _, field_ms, _, trace_ps, _ = prof
+    peak = ctypes.c_double()
+    peak_ms = ctypes.c_double()
+    lib.nufi_fp64_peak(dev, ctypes.byref(peak), ctypes.byref(peak_ms))
+    achieved = ALGO_FLOPS[g.d] * trace_ps / (trace_ms * 1e-3) / 1e12
+    roofline = {
+        "bound": "fp64", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
+        "frac": achieved / peak.value if peak.value else None, "traffic": None,
+        "kernel": "trace_rho_kernel", "algo_flops_per_point_step": ALGO_FLOPS[g.d],
+        "trace_launches": int(trace_launches), "trace_ms_per_launch": trace_ms / max(1, trace_launches),
+        "trace_share_of_run": trace_ms / (trace_ms + reduce_ms + field_ms) if trace_ms else None,
+        "peak_source": "measured in-run: DFMA-chain kernel (nufi_fp64_peak); MEASURED_PEAKS.json has no FP64 entry",
+        "note": "tensor cores not applicable (FP64 gather-stencil, no dense contraction); HBM ~0 (history L2-resident)",
+    }
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_sample(args.config, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": "backtraced point-steps/s (FP64) & wall time to t_end",
+            "value": value, "unit": "point-steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_run, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (deterministic BASELINE config; no dataset)",
+            "config": {"workload": args.config, "description": w.description, "time_steps_per_run": steps_per_run,
+                       "point_steps_per_run": ps_run, "l2": "flushed (256 MiB write) between timed runs",
+                       "parallelism": f"v-block sharding x{world}" if world > 1 else "single GPU"},
+            "wall_s_to_t_end": ms_per_run / 1e3,
+            "e2e": {"value": e2e_value, "unit": "point-steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": d2h,
+                    "api": "Simulation(grid, ic, tau, N).run() -> host numpy rho/E/W/stats per time step"},
+            "gpu_launches": int(steps_per_run * 3),
+            "roofline": roofline,
+            "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+    gpu_arm(args, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

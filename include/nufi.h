@@ -1,0 +1,185 @@
+/*
+ * nufi.h -- C-ABI of the B200-native NuFI hot path (libnufi_b200.so).
+ *
+ * Drop-in boundary for the reference's per-step rho loop
+ * (/root/reference/pkg/src/vpflow).  Plain C types only:
+ * pointers, sizes, doubles.  No torch types cross this boundary.
+ *
+ * Every entry point returns an int status:
+ *   NUFI_OK (0), NUFI_ERR_USAGE (1) -> vpflow UsageError            errors.py:8-9
+ *               NUFI_ERR_NUMERICAL (2) -> NumericalConsistencyError  errors.py:16-17
+ *               NUFI_ERR_CONFIG (3) -> ConfigError                   errors.py:12-13
+ *               NUFI_ERR_CUDA (4), NUFI_ERR_COMM (5)
+ * and nufi_last_error() returns a thread-local message for the last failure.
+ *
+ * Buffers are caller-owned.  Pointer arguments may be host or device memory
+ * (resolved through unified addressing); host outputs are complete when the
+ * call returns, device outputs are ordered on the handle's stream.
+ * One host thread drives one handle; one handle per GPU / rank.
+ */
+#ifndef NUFI_H
+#define NUFI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NUFI_ABI_VERSION 1
+
+#define NUFI_OK 0
+#define NUFI_ERR_USAGE 1
+#define NUFI_ERR_NUMERICAL 2
+#define NUFI_ERR_CONFIG 3
+#define NUFI_ERR_CUDA 4
+#define NUFI_ERR_COMM 5
+
+#define NUFI_MAX_CENTERS 4
+
+/* nufi_trace modes */
+#define NUFI_TRACE_FAST 0   /* production arithmetic (FMA, cell-centred polynomial form) */
+#define NUFI_TRACE_PARITY 1 /* reference operation order, no FMA: bit-exact vs kernels.py */
+
+/* One velocity axis of f0: v^power * sum_m weights[m] * N(v; centers[m], 1).
+ * Mirrors VelocityProfile, initial.py:25-56 (power in {0, 2}, weights > 0). */
+typedef struct nufi_profile {
+    int32_t n_centers;
+    int32_t power;
+    double centers[NUFI_MAX_CENTERS];
+    double weights[NUFI_MAX_CENTERS];
+} nufi_profile;
+
+/* GridSpec (grids.py:18-59) + InitialCondition (initial.py:72-106) + tau
+ * (spline.py:118-120) + the history capacity (PotentialHistory, spline.py:108-155).
+ * rho_bar: background density; NaN -> computed on the device with the
+ * quadrature of background_density (initial.py:187-208).
+ * v_blocks: fixed number B of velocity blocks whose partial sums are combined
+ * in a fixed order (0 -> default); a rank traces blocks [block_lo, block_hi). */
+typedef struct nufi_config {
+    int32_t d;
+    int32_t Nx;
+    int32_t Nv;
+    int32_t n_max; /* largest step index; history capacity n_max + 1 slabs */
+    double L;
+    double vmax;
+    double tau;
+    double alpha;
+    double k;
+    double rho_bar;
+    nufi_profile profiles[3];
+    int32_t v_blocks;
+    int32_t block_lo;
+    int32_t block_hi;
+    int32_t flags; /* reserved, 0 */
+} nufi_config;
+
+typedef struct nufi_handle nufi_handle;
+
+/* ---- lifecycle ----------------------------------------------------------- */
+
+/* Validates cfg like GridSpec.__post_init__ (grids.py:28-34),
+ * VelocityProfile.__post_init__ (initial.py:33-39),
+ * InitialCondition.__post_init__ (initial.py:89-106), PotentialHistory
+ * (spline.py:119-120) and fit_spline's Nx >= 4 (spline.py:73-74); allocates the
+ * device-resident history.  stream: a cudaStream_t, or NULL for a private one. */
+int nufi_create(const nufi_config *cfg, int device, void *stream, nufi_handle **out);
+int nufi_destroy(nufi_handle *h);
+const char *nufi_last_error(void);
+int nufi_abi_version(void);
+int nufi_sync(nufi_handle *h);
+/* background density actually used (FlowContext.rho_bar, flow.py:36-39) */
+int nufi_rho_bar(nufi_handle *h, double *out);
+/* Install the initial condition of cfg (alpha, k, profiles, rho_bar; the grid
+ * fields must match the handle) -- binding a FlowContext to a history. */
+int nufi_set_initial_condition(nufi_handle *h, const nufi_config *cfg);
+/* Grow the history capacity to at least `slabs` (PotentialHistory's doubling
+ * growth, spline.py:136-139; stored rows are preserved). */
+int nufi_reserve(nufi_handle *h, int64_t slabs);
+int64_t nufi_capacity(nufi_handle *h);
+
+/* ---- history (PotentialHistory, spline.py:108-155) ----------------------- */
+
+int nufi_history_len(nufi_handle *h, int64_t *len);
+/* Replace the history by `count` coefficient slabs (count, Nx^d) row-major. */
+int nufi_load_history(nufi_handle *h, const double *coeffs, int64_t count);
+/* Copy slabs [first, first+count) out, (count, Nx^d) row-major. */
+int nufi_get_history(nufi_handle *h, double *coeffs, int64_t first, int64_t count);
+/* PotentialHistory.append(SplineField) (spline.py:132-142): one fitted slab. */
+int nufi_append_coeffs(nufi_handle *h, const double *coeffs);
+/* Drop slabs so that len == count (count <= len). */
+int nufi_truncate_history(nufi_handle *h, int64_t count);
+
+/* ---- the hot path -------------------------------------------------------- */
+
+/* compute_rho (density.py:72-91) for a single rank: traces every quadrature
+ * point of the grid with Psi-tilde through history rows 0..n-1 (needs
+ * len >= n, else NUFI_ERR_USAGE like _require_history, flow.py:55-62),
+ * evaluates f0 at the foot point and reduces over v.
+ * rho_out: Nx^d doubles (neutralised); stats3 = {neutralization, f_min, f_max};
+ * evals (optional) += Nx^d * Nv^d * n (FlowContext.field_evals, flow.py:89). */
+int nufi_rho(nufi_handle *h, int64_t n, double *rho_out, double *stats3, int64_t *evals);
+
+/* Multi-rank split of nufi_rho.  partials: DEVICE buffer of v_blocks * (Nx^d + 2)
+ * doubles: rows [b][Nx^d] of per-block v-sums followed by v_blocks (min, max)
+ * pairs.  This rank writes its blocks [block_lo, block_hi) and zeros elsewhere, so an
+ * elementwise SUM allreduce of the ranks' buffers is exact (one nonzero
+ * contributor per element) and the combine is rank-count independent. */
+int nufi_rho_partials(nufi_handle *h, int64_t n, double *partials, int64_t *evals);
+/* Multi-rank step tail: combine the (allreduced) block partials, neutralise,
+ * then exactly nufi_field_update's work, appending slab n (requires len == n).
+ * Every rank runs it redundantly and so holds the full history. */
+int nufi_step_finish(nufi_handle *h, int64_t n, const double *partials, double *rho_out, double *E_out,
+                     double *W_out, double *stats3);
+/* Fixed-order combine of the (allreduced) block partials -> rho, stats3. */
+int nufi_rho_finish(nufi_handle *h, const double *partials, double *rho_out, double *stats3);
+int64_t nufi_partials_len(nufi_handle *h); /* v_blocks * (Nx^d + 2) */
+
+/* solve_poisson (poisson.py:90-112) + fit_spline (spline.py:71-86) +
+ * PotentialHistory.append (spline.py:132-142) + electric_energy
+ * (poisson.py:115-120) + E at the nodes (SplineField.eval_E_many at
+ * x_node_matrix, spline.py:50-52 / kernels.py:102-123), on the device.
+ * rho: Nx^d neutral densities.  Outputs (optional, NULL to skip):
+ * W_out (1), E_out (Nx^d * d, row-major (node, axis)), coeffs_out (Nx^d).
+ * Returns NUFI_ERR_NUMERICAL (history unchanged) if |mean rho| > 1e-8 max|rho|. */
+int nufi_field_update(nufi_handle *h, const double *rho, double *W_out, double *E_out,
+                      double *coeffs_out);
+
+/* One full step n (requires len == n): nufi_rho + nufi_field_update, all on
+ * the device.  Outputs optional. */
+int nufi_step(nufi_handle *h, int64_t n, double *rho_out, double *E_out, double *W_out,
+              double *stats3, int64_t *evals);
+
+/* The run driver: steps len .. n_last inclusive.
+ * Per-step outputs are written at row (step - first_step) of
+ * rho_hist (Nx^d), E_hist (Nx^d*d), W_hist (1), stats_hist (3); any may be NULL.
+ * Host outputs are copied once at the end. */
+int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, double *W_hist,
+             double *stats_hist, int64_t *evals);
+
+/* trace_backward (kernels.py:390-412) on caller points, in place.
+ * X, V: (M, d) row-major float64 (host or device).  half_kick: Psi (needs
+ * len >= n + 1) vs Psi-tilde (len >= n).  mode: NUFI_TRACE_FAST / _PARITY.
+ * evals (optional) += M * (n + half_kick) for n > 0. */
+int nufi_trace(nufi_handle *h, int64_t n, double *X, double *V, int64_t M, int half_kick, int mode,
+               int64_t *evals);
+
+/* f0 at caller points (eval_f0, initial.py:165-180): F[M]. */
+int nufi_eval_f0(nufi_handle *h, const double *X, const double *V, int64_t M, double *F);
+
+/* ---- measurement ---------------------------------------------------------- */
+
+/* Per-launch CUDA-event timing of the library's kernels on the handle stream.
+ * enable != 0 starts (and zeroes) accumulation; nufi_profiling_read fills
+ * out[8] = {trace_ms, trace_launches, reduce_ms, reduce_launches,
+ *           field_ms, field_launches, trace_point_steps, 0}. */
+int nufi_profiling(nufi_handle *h, int enable);
+int nufi_profiling_read(nufi_handle *h, double *out8);
+/* FP64 vector (DFMA) peak of `device`, measured by a DFMA-chain kernel. */
+int nufi_fp64_peak(int device, double *tflops, double *ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NUFI_H */

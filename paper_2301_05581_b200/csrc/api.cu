@@ -1,0 +1,867 @@
+// api.cu -- the C-ABI of libnufi_b200.so (declared in include/nufi.h).
+//
+// Owns the device-resident potential history (PotentialHistory,
+// spline.py:108-155, preallocated to n_max + 1 slabs instead of doubling),
+// the per-step scratch, and the launch sequence of one NuFI step:
+//   trace_rho (trace + f0 + per-tile v-sums)  -> reduce_blocks (fixed-order
+//   v-block sums) -> [caller's allreduce for multi-rank] -> field_update
+//   (combine, neutralise, Poisson, spline fit, append, W, E).
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "trace_common.cuh"
+
+namespace nufi {
+size_t trace_rho_smem_bytes(const TraceRhoParams &p, int threads);
+cudaError_t launch_trace_rho(int d, int ppt, bool pow2, const TraceRhoParams &p, double K, int ctas, int threads,
+                             cudaStream_t st);
+cudaError_t launch_reduce_blocks(const double *partial, const double *fminmax, double *out, int nodes,
+                                 int node_tiles, int vt_per_block, int b_lo, int b_hi, int B, cudaStream_t st);
+cudaError_t launch_trace_points(int d, int mode, bool pow2, const double *hist, const double *ev_hist,
+                                int ev_slab_elems, int N, int nodes, double L, int n, double tau, double K, double *X,
+                                double *V, int64_t M, int half_kick, cudaStream_t st);
+cudaError_t launch_eval_f0(int d, const F0Params &f0, const double *X, const double *V, int64_t M, double *F,
+                           cudaStream_t st);
+cudaError_t launch_build_ev_slabs(const double *hist, double *ev_hist, int d, int N, int nodes, int ev_slab_elems,
+                                  double K, int64_t r0, int64_t r1, cudaStream_t st);
+}  // namespace nufi
+
+namespace nufi {
+cudaError_t launch_field_update(const FieldParams &p, cudaStream_t st);
+cudaError_t launch_rho_bar(const RhoBarParams &p, cudaStream_t st);
+}  // namespace nufi
+
+using namespace nufi;
+
+// ----------------------------------------------------------------------------
+// errors
+// ----------------------------------------------------------------------------
+
+static thread_local std::string g_last_error;
+
+static int fail(int code, const std::string &msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define CU(expr)                                                                                  \
+    do {                                                                                          \
+        cudaError_t _e = (expr);                                                                  \
+        if (_e != cudaSuccess)                                                                    \
+            return fail(NUFI_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));     \
+    } while (0)
+
+#define CHECK_HANDLE(h)                                                                           \
+    do {                                                                                          \
+        if (!(h)) return fail(NUFI_ERR_USAGE, "null handle");                                     \
+        CU(cudaSetDevice((h)->device));                                                           \
+    } while (0)
+
+// ----------------------------------------------------------------------------
+// handle
+// ----------------------------------------------------------------------------
+
+struct nufi_handle {
+    nufi_config cfg{};
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+
+    int d = 1, N = 0, Nv = 0, nodes = 0;
+    int64_t V = 0;  // Nv^d
+    int64_t cap = 0;
+    bool pow2 = false;
+    double hx = 0, inv_h = 0, hv = 0, hv_d = 0, L_d = 0, K = 0, rho_bar = 0;
+    F0Params f0{};
+
+    // v-blocks and CTA tiling
+    int B = 1, b_lo = 0, b_hi = 1;
+    int threads = 128, ppt = 1, passes = 1, vt_rows = 4, vt_total = 1, vt_per_block = 1, node_tiles = 1;
+    int sps = 1, stages = 2, ev_elems = 0;
+
+    // device buffers
+    double *hist = nullptr, *ev_hist = nullptr;
+    double *partial = nullptr, *fminmax = nullptr, *blocks = nullptr;
+    double *d_rho = nullptr, *d_E = nullptr, *d_W = nullptr, *d_stats = nullptr, *d_rho_bar = nullptr;
+    int *d_status = nullptr;
+    int64_t *d_len = nullptr;
+    // run outputs (device) and their pinned host staging
+    double *run_dev = nullptr, *run_host = nullptr;
+    size_t run_elems = 0;
+
+    int64_t len = 0;  // host mirror of the history length
+
+    // optional per-launch event timing (nufi_profile)
+    bool profiling = false;
+    struct Pending {
+        cudaEvent_t a, b;
+        int kind;  // 0 trace, 1 reduce, 2 field
+        double point_steps;
+    };
+    std::vector<Pending> pending;
+    double prof[8] = {0};
+};
+
+// Record events around one launch when profiling (resolved lazily by nufi_profile_read).
+struct ProfScope {
+    nufi_handle *h;
+    int kind;
+    double ps;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(nufi_handle *h_, int kind_, double ps_ = 0) : h(h_), kind(kind_), ps(ps_) {
+        if (h->profiling) {
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            cudaEventRecord(a, h->stream);
+        }
+    }
+    ~ProfScope() {
+        if (h->profiling) {
+            cudaEventRecord(b, h->stream);
+            h->pending.push_back({a, b, kind, ps});
+        }
+    }
+};
+
+static bool is_device_ptr(const void *p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static int ipow(int b, int e) {
+    int r = 1;
+    for (int i = 0; i < e; ++i) r *= b;
+    return r;
+}
+
+// Reference validation rules.
+static int validate(const nufi_config &c) {
+    char buf[256];
+    if (c.d < 1 || c.d > 3) {
+        snprintf(buf, sizeof buf, "dimension must be 1, 2 or 3, got %d", c.d);  // grids.py:28-29
+        return fail(NUFI_ERR_USAGE, buf);
+    }
+    if (c.Nx < 2 || c.Nv < 2) {
+        snprintf(buf, sizeof buf, "need Nx >= 2 and Nv >= 2, got Nx=%d, Nv=%d", c.Nx, c.Nv);  // grids.py:30-31
+        return fail(NUFI_ERR_USAGE, buf);
+    }
+    if (!(c.L > 0 && c.vmax > 0)) {
+        snprintf(buf, sizeof buf, "need L > 0 and vmax > 0, got L=%g, vmax=%g", c.L, c.vmax);  // grids.py:32-33
+        return fail(NUFI_ERR_USAGE, buf);
+    }
+    if (c.Nx < 4) {
+        snprintf(buf, sizeof buf, "spline fitting needs Nx >= 4, got %d", c.Nx);  // spline.py:73-74
+        return fail(NUFI_ERR_USAGE, buf);
+    }
+    if (!(c.tau > 0)) {
+        snprintf(buf, sizeof buf, "time step must be positive, got %g", c.tau);  // spline.py:119-120
+        return fail(NUFI_ERR_USAGE, buf);
+    }
+    if (c.n_max < 0) return fail(NUFI_ERR_USAGE, "n_max must be >= 0");
+    for (int a = 0; a < c.d; ++a) {
+        const nufi_profile &p = c.profiles[a];
+        if (p.n_centers < 1 || p.n_centers > NUFI_MAX_CENTERS)
+            return fail(NUFI_ERR_USAGE, "centers and weights must be non-empty and equal-length");  // initial.py:33-34
+        if (p.power != 0 && p.power != 2) {
+            snprintf(buf, sizeof buf, "velocity power must be 0 or 2, got %d", p.power);  // initial.py:35-36
+            return fail(NUFI_ERR_USAGE, buf);
+        }
+        for (int m = 0; m < p.n_centers; ++m)
+            if (!(p.weights[m] > 0)) return fail(NUFI_ERR_USAGE, "mixture weights must be positive");  // initial.py:37-38
+    }
+    if (c.alpha < 0) {
+        snprintf(buf, sizeof buf, "perturbation amplitude must be >= 0, got %g", c.alpha);  // initial.py:91-92
+        return fail(NUFI_ERR_USAGE, buf);
+    }
+    if (c.alpha * c.d > 1.0 + 1e-12) {
+        snprintf(buf, sizeof buf, "alpha*d = %g > 1 makes f0 negative", c.alpha * c.d);  // initial.py:93-94
+        return fail(NUFI_ERR_USAGE, buf);
+    }
+    const double cycles = c.k * c.L / (2.0 * M_PI);
+    if (std::fabs(cycles - std::round(cycles)) > 1e-9) {
+        snprintf(buf, sizeof buf, "k*L = %g is not a multiple of 2*pi; f0 would not be x-periodic", c.k * c.L);
+        return fail(NUFI_ERR_USAGE, buf);  // initial.py:95-99
+    }
+    const long long nodes = (long long)std::pow((double)c.Nx, c.d);
+    if (nodes > MAX_FIELD_NODES) {
+        snprintf(buf, sizeof buf, "Nx^d = %lld exceeds the single-CTA field update limit %d", nodes, MAX_FIELD_NODES);
+        return fail(NUFI_ERR_CONFIG, buf);
+    }
+    const double V = std::pow((double)c.Nv, c.d);
+    if (V * (double)nodes > 9.0e15) return fail(NUFI_ERR_CONFIG, "too many quadrature points");
+    return NUFI_OK;
+}
+
+// CTA tiling: v-rows per CTA tile = warps * ppt * passes must divide V / B.
+static void choose_tiling(nufi_handle *h) {
+    const int64_t per_block = h->V / h->B;
+    int warps, ppt, passes;
+    if (h->d == 1) {
+        warps = 4, ppt = 1, passes = 1;
+    } else if (h->d == 2) {
+        warps = 8, ppt = 1, passes = 1;
+    } else {
+        warps = 8, ppt = 1, passes = 4;
+    }
+    while (warps > 1 && (per_block % (warps * ppt) != 0)) warps >>= 1;
+    while (ppt > 1 && (per_block % (warps * ppt) != 0)) ppt >>= 1;
+    while (passes > 1 && (per_block % ((int64_t)warps * ppt * passes) != 0)) passes >>= 1;
+    if (per_block % ((int64_t)warps * ppt * passes) != 0) warps = ppt = passes = 1;
+    h->threads = warps * 32;
+    h->ppt = ppt;
+    h->passes = passes;
+    h->vt_rows = warps * ppt * passes;
+    h->vt_total = (int)(h->V / h->vt_rows);
+    h->vt_per_block = (int)(per_block / h->vt_rows);
+    h->node_tiles = (h->nodes + 31) / 32;
+    // TMA ring: slabs per stage and stage count
+    const int slab_bytes = h->ev_elems * 8;
+    if (h->d == 1) {
+        h->sps = std::max(1, std::min(16, 24576 / slab_bytes));
+        h->stages = 3;
+    } else if (h->d == 2) {
+        h->sps = std::max(1, 16384 / slab_bytes);
+        h->stages = 3;
+    } else {
+        h->sps = std::max(1, 32768 / slab_bytes);
+        h->stages = 2;
+    }
+}
+
+// f0 descriptor + background density (initial.py:165-180, 187-208)
+static int install_ic(nufi_handle *h, const nufi_config &c) {
+    h->cfg.alpha = c.alpha;
+    h->cfg.k = c.k;
+    h->cfg.rho_bar = c.rho_bar;
+    for (int a = 0; a < 3; ++a) h->cfg.profiles[a] = c.profiles[a];
+    h->f0 = F0Params{};
+    h->f0.d = c.d;
+    h->f0.alpha = c.alpha;
+    h->f0.k = c.k;
+    for (int a = 0; a < c.d; ++a) {
+        h->f0.n_centers[a] = c.profiles[a].n_centers;
+        h->f0.power[a] = c.profiles[a].power;
+        for (int m = 0; m < NUFI_MAX_CENTERS; ++m) {
+            h->f0.centers[a][m] = c.profiles[a].centers[m];
+            h->f0.weights[a][m] = c.profiles[a].weights[m];
+        }
+    }
+    if (std::isnan(c.rho_bar)) {
+        RhoBarParams rp{};
+        rp.d = c.d;
+        rp.N = c.Nx;
+        rp.Nv = c.Nv;
+        rp.hx = h->hx;
+        rp.hv = h->hv;
+        rp.vmax = c.vmax;
+        rp.hx_d = std::pow(h->hx, (double)c.d);
+        rp.hv_d = h->hv_d;
+        rp.L_d = h->L_d;
+        rp.f0 = h->f0;
+        rp.out = h->d_rho_bar;
+        CU(launch_rho_bar(rp, h->stream));
+        CU(cudaMemcpyAsync(&h->rho_bar, h->d_rho_bar, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CU(cudaStreamSynchronize(h->stream));
+    } else {
+        h->rho_bar = c.rho_bar;
+    }
+    return NUFI_OK;
+}
+
+static int grow(nufi_handle *h, int64_t cap) {
+    if (cap <= h->cap) return NUFI_OK;
+    double *nh = nullptr, *ne = nullptr;
+    CU(cudaMalloc(&nh, cap * (size_t)h->nodes * sizeof(double)));
+    CU(cudaMalloc(&ne, cap * (size_t)h->ev_elems * sizeof(double)));
+    if (h->len > 0) {
+        CU(cudaMemcpyAsync(nh, h->hist, h->len * (size_t)h->nodes * sizeof(double), cudaMemcpyDeviceToDevice,
+                           h->stream));
+        CU(cudaMemcpyAsync(ne, h->ev_hist, h->len * (size_t)h->ev_elems * sizeof(double), cudaMemcpyDeviceToDevice,
+                           h->stream));
+    }
+    CU(cudaStreamSynchronize(h->stream));
+    cudaFree(h->hist);
+    cudaFree(h->ev_hist);
+    h->hist = nh;
+    h->ev_hist = ne;
+    h->cap = cap;
+    h->cfg.n_max = (int32_t)(cap - 1);
+    return NUFI_OK;
+}
+
+extern "C" {
+
+int nufi_set_initial_condition(nufi_handle *h, const nufi_config *cfg) {
+    CHECK_HANDLE(h);
+    if (!cfg) return fail(NUFI_ERR_USAGE, "null config");
+    if (cfg->d != h->cfg.d || cfg->Nx != h->cfg.Nx || cfg->Nv != h->cfg.Nv || cfg->L != h->cfg.L ||
+        cfg->vmax != h->cfg.vmax)
+        return fail(NUFI_ERR_USAGE, "initial condition grid does not match the history grid");
+    nufi_config c = h->cfg;
+    c.alpha = cfg->alpha;
+    c.k = cfg->k;
+    c.rho_bar = cfg->rho_bar;
+    for (int a = 0; a < 3; ++a) c.profiles[a] = cfg->profiles[a];
+    int rc = validate(c);
+    if (rc) return rc;
+    return install_ic(h, c);
+}
+
+int nufi_reserve(nufi_handle *h, int64_t slabs) {
+    CHECK_HANDLE(h);
+    if (slabs > (int64_t)1 << 30) return fail(NUFI_ERR_USAGE, "capacity too large");
+    return grow(h, slabs);
+}
+
+int64_t nufi_capacity(nufi_handle *h) { return h ? h->cap : 0; }
+
+const char *nufi_last_error(void) { return g_last_error.c_str(); }
+int nufi_abi_version(void) { return NUFI_ABI_VERSION; }
+
+int nufi_create(const nufi_config *cfg, int device, void *stream, nufi_handle **out) {
+    if (!cfg || !out) return fail(NUFI_ERR_USAGE, "null argument");
+    *out = nullptr;
+    int rc = validate(*cfg);
+    if (rc) return rc;
+    int ndev = 0;
+    CU(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(NUFI_ERR_USAGE, "invalid device index");
+    CU(cudaSetDevice(device));
+
+    nufi_handle *h = new nufi_handle();
+    h->cfg = *cfg;
+    h->device = device;
+    if (stream) {
+        h->stream = (cudaStream_t)stream;
+    } else {
+        CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        h->own_stream = true;
+    }
+    const nufi_config &c = *cfg;
+    h->d = c.d;
+    h->N = c.Nx;
+    h->Nv = c.Nv;
+    h->nodes = ipow(c.Nx, c.d);
+    h->V = 1;
+    for (int a = 0; a < c.d; ++a) h->V *= c.Nv;
+    h->cap = (int64_t)c.n_max + 1;
+    h->pow2 = (c.Nx & (c.Nx - 1)) == 0;
+    h->hx = c.L / c.Nx;                       // grids.py:37-38
+    h->hv = 2.0 * c.vmax / c.Nv;              // grids.py:41-42
+    h->inv_h = (double)c.Nx / c.L;            // kernels.py:187
+    h->hv_d = std::pow(h->hv, (double)c.d);   // density.py:75
+    h->L_d = std::pow(c.L, (double)c.d);      // poisson.py:120
+    h->K = -(c.tau * c.tau) * (h->inv_h * h->inv_h);
+    // v-blocks (fixed combine order, independent of the rank count)
+    int B = c.v_blocks > 0 ? c.v_blocks : 8;
+    while (B > 1 && (h->V % B != 0)) --B;
+    if (c.v_blocks > 0 && B != c.v_blocks) {
+        delete h;
+        return fail(NUFI_ERR_USAGE, "v_blocks must divide Nv^d");
+    }
+    h->B = B;
+    h->b_lo = c.block_hi > c.block_lo ? c.block_lo : 0;
+    h->b_hi = c.block_hi > c.block_lo ? c.block_hi : B;
+    if (h->b_lo < 0 || h->b_hi > B) {
+        delete h;
+        return fail(NUFI_ERR_USAGE, "block range outside [0, v_blocks)");
+    }
+    h->ev_elems = ev_slab_elems(c.d, c.Nx);
+    choose_tiling(h);
+
+    const size_t nodes = h->nodes;
+    CU(cudaMalloc(&h->hist, h->cap * nodes * sizeof(double)));
+    CU(cudaMalloc(&h->ev_hist, h->cap * (size_t)h->ev_elems * sizeof(double)));
+    CU(cudaMalloc(&h->partial, (size_t)h->vt_total * nodes * sizeof(double)));
+    CU(cudaMalloc(&h->fminmax, (size_t)h->vt_total * h->node_tiles * 2 * sizeof(double)));
+    CU(cudaMalloc(&h->blocks, ((size_t)h->B * nodes + 2 * h->B) * sizeof(double)));
+    CU(cudaMalloc(&h->d_rho, nodes * sizeof(double)));
+    CU(cudaMalloc(&h->d_E, nodes * c.d * sizeof(double)));
+    CU(cudaMalloc(&h->d_W, 8 * sizeof(double)));
+    CU(cudaMalloc(&h->d_stats, 8 * sizeof(double)));
+    CU(cudaMalloc(&h->d_rho_bar, sizeof(double)));
+    CU(cudaMalloc(&h->d_status, sizeof(int)));
+    CU(cudaMalloc(&h->d_len, sizeof(int64_t)));
+    CU(cudaMemsetAsync(h->d_status, 0, sizeof(int), h->stream));
+    CU(cudaMemsetAsync(h->d_len, 0, sizeof(int64_t), h->stream));
+
+    rc = install_ic(h, c);
+    if (rc) {
+        nufi_destroy(h);
+        return rc;
+    }
+    *out = h;
+    return NUFI_OK;
+}
+
+int nufi_destroy(nufi_handle *h) {
+    if (!h) return NUFI_OK;
+    cudaSetDevice(h->device);
+    cudaStreamSynchronize(h->stream);
+    for (void *p : {(void *)h->hist, (void *)h->ev_hist, (void *)h->partial, (void *)h->fminmax, (void *)h->blocks,
+                    (void *)h->d_rho, (void *)h->d_E, (void *)h->d_W, (void *)h->d_stats, (void *)h->d_rho_bar,
+                    (void *)h->d_status, (void *)h->d_len, (void *)h->run_dev})
+        if (p) cudaFree(p);
+    if (h->run_host) cudaFreeHost(h->run_host);
+    if (h->own_stream) cudaStreamDestroy(h->stream);
+    delete h;
+    return NUFI_OK;
+}
+
+int nufi_sync(nufi_handle *h) {
+    CHECK_HANDLE(h);
+    CU(cudaStreamSynchronize(h->stream));
+    return NUFI_OK;
+}
+
+int nufi_rho_bar(nufi_handle *h, double *out) {
+    if (!h || !out) return fail(NUFI_ERR_USAGE, "null argument");
+    *out = h->rho_bar;
+    return NUFI_OK;
+}
+
+int64_t nufi_partials_len(nufi_handle *h) { return h ? (int64_t)h->B * h->nodes + 2 * h->B : 0; }
+
+// ---- history --------------------------------------------------------------
+
+int nufi_history_len(nufi_handle *h, int64_t *len) {
+    if (!h || !len) return fail(NUFI_ERR_USAGE, "null argument");
+    *len = h->len;
+    return NUFI_OK;
+}
+
+int nufi_load_history(nufi_handle *h, const double *coeffs, int64_t count) {
+    CHECK_HANDLE(h);
+    if (count < 0 || count > h->cap) return fail(NUFI_ERR_USAGE, "history count exceeds the capacity n_max + 1");
+    if (count > 0 && !coeffs) return fail(NUFI_ERR_USAGE, "null coefficients");
+    if (count > 0) {
+        CU(cudaMemcpyAsync(h->hist, coeffs, (size_t)count * h->nodes * sizeof(double), cudaMemcpyDefault, h->stream));
+        CU(launch_build_ev_slabs(h->hist, h->ev_hist, h->d, h->N, h->nodes, h->ev_elems, h->K, 0, count, h->stream));
+    }
+    h->len = count;
+    CU(cudaMemcpyAsync(h->d_len, &h->len, sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    return NUFI_OK;
+}
+
+int nufi_get_history(nufi_handle *h, double *coeffs, int64_t first, int64_t count) {
+    CHECK_HANDLE(h);
+    if (first < 0 || count < 0 || first + count > h->len)
+        return fail(NUFI_ERR_USAGE, "requested rows outside the stored history");
+    if (count == 0) return NUFI_OK;
+    CU(cudaMemcpyAsync(coeffs, h->hist + (size_t)first * h->nodes, (size_t)count * h->nodes * sizeof(double),
+                       cudaMemcpyDefault, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    return NUFI_OK;
+}
+
+int nufi_append_coeffs(nufi_handle *h, const double *coeffs) {
+    CHECK_HANDLE(h);
+    if (!coeffs) return fail(NUFI_ERR_USAGE, "null coefficients");
+    if (h->len >= h->cap) return fail(NUFI_ERR_USAGE, "history is full (capacity n_max + 1)");
+    CU(cudaMemcpyAsync(h->hist + (size_t)h->len * h->nodes, coeffs, (size_t)h->nodes * sizeof(double),
+                       cudaMemcpyDefault, h->stream));
+    CU(launch_build_ev_slabs(h->hist, h->ev_hist, h->d, h->N, h->nodes, h->ev_elems, h->K, h->len, h->len + 1,
+                             h->stream));
+    h->len += 1;
+    CU(cudaStreamSynchronize(h->stream));
+    return NUFI_OK;
+}
+
+int nufi_truncate_history(nufi_handle *h, int64_t count) {
+    if (!h) return fail(NUFI_ERR_USAGE, "null handle");
+    if (count < 0 || count > h->len) return fail(NUFI_ERR_USAGE, "truncate beyond the stored history");
+    h->len = count;
+    return NUFI_OK;
+}
+
+}  // extern "C"
+
+// ---- internal step pieces -------------------------------------------------
+
+// trace + per-tile sums for blocks [b_lo, b_hi) -> out (B*nodes sums + 2B min/max)
+static int enqueue_partials(nufi_handle *h, int64_t n, int b_lo, int b_hi, double *out) {
+    if (b_hi <= b_lo) return NUFI_OK;
+    TraceRhoParams p{};
+    p.N = h->N;
+    p.nodes = h->nodes;
+    p.Nv = h->Nv;
+    p.V = h->V;
+    p.node_tiles = h->node_tiles;
+    p.vt_rows = h->vt_rows;
+    p.passes = h->passes;
+    p.vt_lo = b_lo * h->vt_per_block;
+    p.n = (int)n;
+    p.hx = h->hx;
+    p.inv_h = h->inv_h;
+    p.vmax = h->cfg.vmax;
+    p.hv = h->hv;
+    p.vel_to_scaled = h->cfg.tau * h->inv_h;
+    p.scaled_to_vel = 1.0 / p.vel_to_scaled;
+    p.ev_hist = h->ev_hist;
+    p.ev_slab_elems = h->ev_elems;
+    p.slabs_per_stage = h->sps;
+    p.stages = h->stages;
+    p.f0 = h->f0;
+    p.partial = h->partial;
+    p.fminmax = h->fminmax;
+    const int ctas = (b_hi - b_lo) * h->vt_per_block * h->node_tiles;
+    {
+        ProfScope ps(h, 0, (double)h->nodes * (double)(h->V / h->B) * (b_hi - b_lo) * (double)n);
+        CU(launch_trace_rho(h->d, h->ppt, h->pow2, p, h->K, ctas, h->threads, h->stream));
+    }
+    {
+        ProfScope ps(h, 1);
+        CU(launch_reduce_blocks(h->partial, h->fminmax, out, h->nodes, h->node_tiles, h->vt_per_block, b_lo, b_hi,
+                                h->B, h->stream));
+    }
+    return NUFI_OK;
+}
+
+static FieldParams field_params(nufi_handle *h) {
+    FieldParams f{};
+    f.d = h->d;
+    f.N = h->N;
+    f.nodes = h->nodes;
+    f.B = h->B;
+    f.L = h->cfg.L;
+    f.inv_h = h->inv_h;
+    f.hv_d = h->hv_d;
+    f.rho_bar = h->rho_bar;
+    f.L_d = h->L_d;
+    f.K = h->K;
+    f.k_scale = 2.0 * M_PI / h->cfg.L;
+    f.hist = h->hist;
+    f.ev_hist = h->ev_hist;
+    f.ev_slab_elems = h->ev_elems;
+    f.status = h->d_status;
+    f.hist_len = h->d_len;
+    return f;
+}
+
+static int copy_out(nufi_handle *h, void *dst, const void *src, size_t bytes) {
+    if (dst) CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, h->stream));
+    return NUFI_OK;
+}
+
+static int check_status(nufi_handle *h, const char *what) {
+    int st = 0;
+    CU(cudaMemcpyAsync(&st, h->d_status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    if (st == NUFI_ERR_NUMERICAL) {
+        CU(cudaMemsetAsync(h->d_status, 0, sizeof(int), h->stream));
+        return fail(NUFI_ERR_NUMERICAL, std::string(what) +
+                                            ": density is not neutral: nodal mean exceeds 1e-8 max|rho|; "
+                                            "subtract the mean before solving");
+    }
+    return NUFI_OK;
+}
+
+extern "C" {
+
+int nufi_rho_partials(nufi_handle *h, int64_t n, double *partials, int64_t *evals) {
+    CHECK_HANDLE(h);
+    if (n < 0) return fail(NUFI_ERR_USAGE, "step index must be >= 0");
+    if (n > 0 && h->len < n) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "psi_tilde at step %lld needs fields 0..%lld; history holds %lld", (long long)n,
+                 (long long)(n - 1), (long long)h->len);  // flow.py:55-62
+        return fail(NUFI_ERR_USAGE, buf);
+    }
+    if (!is_device_ptr(partials)) return fail(NUFI_ERR_USAGE, "partials must be a device buffer");
+    CU(cudaMemsetAsync(partials, 0, nufi_partials_len(h) * sizeof(double), h->stream));
+    int rc = enqueue_partials(h, n, h->b_lo, h->b_hi, partials);
+    if (rc) return rc;
+    if (evals) *evals += (int64_t)h->nodes * (h->V / h->B) * (h->b_hi - h->b_lo) * n;
+    return NUFI_OK;
+}
+
+int nufi_rho_finish(nufi_handle *h, const double *partials, double *rho_out, double *stats3) {
+    CHECK_HANDLE(h);
+    if (!is_device_ptr(partials)) return fail(NUFI_ERR_USAGE, "partials must be a device buffer");
+    FieldParams f = field_params(h);
+    f.partials = partials;
+    f.rho_out = h->d_rho;
+    f.stats_out = h->d_stats;
+    f.finish_only = 1;
+    {
+        ProfScope ps(h, 2);
+        CU(launch_field_update(f, h->stream));
+    }
+    int rc = copy_out(h, rho_out, h->d_rho, h->nodes * sizeof(double));
+    if (!rc) rc = copy_out(h, stats3, h->d_stats, 3 * sizeof(double));
+    if (rc) return rc;
+    CU(cudaStreamSynchronize(h->stream));
+    return NUFI_OK;
+}
+
+int nufi_rho(nufi_handle *h, int64_t n, double *rho_out, double *stats3, int64_t *evals) {
+    CHECK_HANDLE(h);
+    if (n < 0) return fail(NUFI_ERR_USAGE, "step index must be >= 0");
+    if (n > 0 && h->len < n) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "psi_tilde at step %lld needs fields 0..%lld; history holds %lld", (long long)n,
+                 (long long)(n - 1), (long long)h->len);
+        return fail(NUFI_ERR_USAGE, buf);
+    }
+    int rc = enqueue_partials(h, n, 0, h->B, h->blocks);
+    if (rc) return rc;
+    if (evals) *evals += (int64_t)h->nodes * h->V * n;
+    return nufi_rho_finish(h, h->blocks, rho_out, stats3);
+}
+
+int nufi_field_update(nufi_handle *h, const double *rho, double *W_out, double *E_out, double *coeffs_out) {
+    CHECK_HANDLE(h);
+    if (!rho) return fail(NUFI_ERR_USAGE, "null rho");
+    if (h->len >= h->cap) return fail(NUFI_ERR_USAGE, "history is full (capacity n_max + 1)");
+    CU(cudaMemcpyAsync(h->d_rho, rho, h->nodes * sizeof(double), cudaMemcpyDefault, h->stream));
+    FieldParams f = field_params(h);
+    f.rho_in = h->d_rho;
+    f.slot = h->len;
+    f.W_out = h->d_W;
+    f.E_out = h->d_E;
+    {
+        ProfScope ps(h, 2);
+        CU(launch_field_update(f, h->stream));
+    }
+    int rc = check_status(h, "solve_poisson");
+    if (rc) return rc;
+    h->len += 1;
+    rc = copy_out(h, W_out, h->d_W, sizeof(double));
+    if (!rc) rc = copy_out(h, E_out, h->d_E, (size_t)h->nodes * h->d * sizeof(double));
+    if (!rc) rc = copy_out(h, coeffs_out, h->hist + (size_t)(h->len - 1) * h->nodes, h->nodes * sizeof(double));
+    if (rc) return rc;
+    CU(cudaStreamSynchronize(h->stream));
+    return NUFI_OK;
+}
+
+int nufi_step(nufi_handle *h, int64_t n, double *rho_out, double *E_out, double *W_out, double *stats3,
+              int64_t *evals) {
+    CHECK_HANDLE(h);
+    if (n != h->len) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "step %lld requires a history of exactly %lld fields, have %lld", (long long)n,
+                 (long long)n, (long long)h->len);
+        return fail(NUFI_ERR_USAGE, buf);
+    }
+    if (n >= h->cap) return fail(NUFI_ERR_USAGE, "history is full (capacity n_max + 1)");
+    int rc = enqueue_partials(h, n, 0, h->B, h->blocks);
+    if (rc) return rc;
+    FieldParams f = field_params(h);
+    f.partials = h->blocks;
+    f.slot = n;
+    f.rho_out = h->d_rho;
+    f.stats_out = h->d_stats;
+    f.W_out = h->d_W;
+    f.E_out = h->d_E;
+    {
+        ProfScope ps(h, 2);
+        CU(launch_field_update(f, h->stream));
+    }
+    rc = check_status(h, "solve_poisson");
+    if (rc) return rc;
+    h->len += 1;
+    if (evals) *evals += (int64_t)h->nodes * h->V * n;
+    rc = copy_out(h, rho_out, h->d_rho, h->nodes * sizeof(double));
+    if (!rc) rc = copy_out(h, E_out, h->d_E, (size_t)h->nodes * h->d * sizeof(double));
+    if (!rc) rc = copy_out(h, W_out, h->d_W, sizeof(double));
+    if (!rc) rc = copy_out(h, stats3, h->d_stats, 3 * sizeof(double));
+    if (rc) return rc;
+    CU(cudaStreamSynchronize(h->stream));
+    return NUFI_OK;
+}
+
+int nufi_step_finish(nufi_handle *h, int64_t n, const double *partials, double *rho_out, double *E_out,
+                     double *W_out, double *stats3) {
+    CHECK_HANDLE(h);
+    if (n != h->len) return fail(NUFI_ERR_USAGE, "step_finish requires len == n");
+    if (n >= h->cap) return fail(NUFI_ERR_USAGE, "history is full (capacity n_max + 1)");
+    if (!is_device_ptr(partials)) return fail(NUFI_ERR_USAGE, "partials must be a device buffer");
+    FieldParams f = field_params(h);
+    f.partials = partials;
+    f.slot = n;
+    f.rho_out = h->d_rho;
+    f.stats_out = h->d_stats;
+    f.W_out = h->d_W;
+    f.E_out = h->d_E;
+    {
+        ProfScope ps(h, 2);
+        CU(launch_field_update(f, h->stream));
+    }
+    int rc = check_status(h, "solve_poisson");
+    if (rc) return rc;
+    h->len += 1;
+    rc = copy_out(h, rho_out, h->d_rho, h->nodes * sizeof(double));
+    if (!rc) rc = copy_out(h, E_out, h->d_E, (size_t)h->nodes * h->d * sizeof(double));
+    if (!rc) rc = copy_out(h, W_out, h->d_W, sizeof(double));
+    if (!rc) rc = copy_out(h, stats3, h->d_stats, 3 * sizeof(double));
+    if (rc) return rc;
+    CU(cudaStreamSynchronize(h->stream));
+    return NUFI_OK;
+}
+
+int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, double *W_hist, double *stats_hist,
+             int64_t *evals) {
+    CHECK_HANDLE(h);
+    const int64_t first = h->len;
+    if (n_last < first) return NUFI_OK;
+    if (n_last >= h->cap) return fail(NUFI_ERR_USAGE, "n_last exceeds n_max");
+    const int64_t steps = n_last - first + 1;
+    const size_t nodes = h->nodes, d = h->d;
+    const size_t per_step = nodes + nodes * d + 1 + 3;  // rho, E, W, stats
+    // device output rows: caller's device buffers directly, else internal + pinned staging
+    const bool dev[4] = {is_device_ptr(rho_hist), is_device_ptr(E_hist), is_device_ptr(W_hist),
+                         is_device_ptr(stats_hist)};
+    const size_t need = (size_t)steps * per_step;
+    if (need > h->run_elems) {
+        if (h->run_dev) cudaFree(h->run_dev);
+        if (h->run_host) cudaFreeHost(h->run_host);
+        h->run_dev = nullptr;
+        h->run_host = nullptr;
+        CU(cudaMalloc(&h->run_dev, need * sizeof(double)));
+        CU(cudaMallocHost(&h->run_host, need * sizeof(double)));
+        h->run_elems = need;
+    }
+    double *base_dev[4] = {h->run_dev, h->run_dev + steps * nodes, h->run_dev + steps * (nodes + nodes * d),
+                           h->run_dev + steps * (nodes + nodes * d + 1)};
+    double *base_host[4] = {h->run_host, h->run_host + steps * nodes, h->run_host + steps * (nodes + nodes * d),
+                            h->run_host + steps * (nodes + nodes * d + 1)};
+    double *user[4] = {rho_hist, E_hist, W_hist, stats_hist};
+    const size_t width[4] = {nodes, nodes * d, 1, 3};
+    for (int q = 0; q < 4; ++q)
+        if (dev[q]) base_dev[q] = user[q];
+
+    for (int64_t n = first; n <= n_last; ++n) {
+        const int64_t row = n - first;
+        int rc = enqueue_partials(h, n, 0, h->B, h->blocks);
+        if (rc) return rc;
+        FieldParams f = field_params(h);
+        f.partials = h->blocks;
+        f.slot = n;
+        f.rho_out = base_dev[0] + row * width[0];
+        f.E_out = base_dev[1] + row * width[1];
+        f.W_out = base_dev[2] + row * width[2];
+        f.stats_out = base_dev[3] + row * width[3];
+        {
+        ProfScope ps(h, 2);
+        CU(launch_field_update(f, h->stream));
+    }
+        // per-step device -> pinned host copies of host-bound outputs (async)
+        for (int q = 0; q < 4; ++q)
+            if (user[q] && !dev[q])
+                CU(cudaMemcpyAsync(base_host[q] + row * width[q], base_dev[q] + row * width[q],
+                                   width[q] * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    }
+    int rc = check_status(h, "solve_poisson");  // synchronises
+    if (rc) return rc;
+    h->len = n_last + 1;
+    for (int q = 0; q < 4; ++q)
+        if (user[q] && !dev[q]) memcpy(user[q], base_host[q], steps * width[q] * sizeof(double));
+    if (evals) *evals += (int64_t)h->nodes * h->V * ((n_last * (n_last + 1) - (first - 1) * first) / 2);
+    return NUFI_OK;
+}
+
+int nufi_profiling(nufi_handle *h, int enable) {
+    CHECK_HANDLE(h);
+    CU(cudaStreamSynchronize(h->stream));
+    for (auto &p : h->pending) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    h->pending.clear();
+    for (double &v : h->prof) v = 0;
+    h->profiling = enable != 0;
+    return NUFI_OK;
+}
+
+int nufi_profiling_read(nufi_handle *h, double *out8) {
+    CHECK_HANDLE(h);
+    CU(cudaStreamSynchronize(h->stream));
+    for (auto &p : h->pending) {
+        float ms = 0;
+        CU(cudaEventElapsedTime(&ms, p.a, p.b));
+        h->prof[2 * p.kind] += ms;
+        h->prof[2 * p.kind + 1] += 1;
+        if (p.kind == 0) h->prof[6] += p.point_steps;
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    h->pending.clear();
+    for (int i = 0; i < 8; ++i) out8[i] = h->prof[i];
+    return NUFI_OK;
+}
+
+int nufi_trace(nufi_handle *h, int64_t n, double *X, double *V, int64_t M, int half_kick, int mode, int64_t *evals) {
+    CHECK_HANDLE(h);
+    if (n < 0) return fail(NUFI_ERR_USAGE, "step index must be >= 0");
+    if (mode != NUFI_TRACE_FAST && mode != NUFI_TRACE_PARITY) return fail(NUFI_ERR_USAGE, "unknown trace mode");
+    if (n == 0) return NUFI_OK;  // kernels.py:397-398
+    const int64_t need = half_kick ? n + 1 : n;
+    if (h->len < need) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "need %lld stored fields for step %lld, have %lld", (long long)need, (long long)n,
+                 (long long)h->len);  // kernels.py:399-402
+        return fail(NUFI_ERR_USAGE, buf);
+    }
+    if (M == 0) return NUFI_OK;  // kernels.py:403-404
+    if (!X || !V) return fail(NUFI_ERR_USAGE, "null points");
+    const size_t bytes = (size_t)M * h->d * sizeof(double);
+    double *dX = X, *dV = V;
+    const bool dx = is_device_ptr(X), dv = is_device_ptr(V);
+    if (!dx) CU(cudaMallocAsync(&dX, bytes, h->stream));
+    if (!dv) CU(cudaMallocAsync(&dV, bytes, h->stream));
+    if (!dx) CU(cudaMemcpyAsync(dX, X, bytes, cudaMemcpyHostToDevice, h->stream));
+    if (!dv) CU(cudaMemcpyAsync(dV, V, bytes, cudaMemcpyHostToDevice, h->stream));
+    CU(launch_trace_points(h->d, mode, h->pow2, h->hist, h->ev_hist, h->ev_elems, h->N, h->nodes, h->cfg.L, (int)n,
+                           h->cfg.tau, h->K, dX, dV, M, half_kick ? 1 : 0, h->stream));
+    if (!dx) CU(cudaMemcpyAsync(X, dX, bytes, cudaMemcpyDeviceToHost, h->stream));
+    if (!dv) CU(cudaMemcpyAsync(V, dV, bytes, cudaMemcpyDeviceToHost, h->stream));
+    if (!dx) CU(cudaFreeAsync(dX, h->stream));
+    if (!dv) CU(cudaFreeAsync(dV, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    if (evals) *evals += M * need;
+    return NUFI_OK;
+}
+
+int nufi_eval_f0(nufi_handle *h, const double *X, const double *V, int64_t M, double *F) {
+    CHECK_HANDLE(h);
+    if (M == 0) return NUFI_OK;
+    if (!X || !V || !F) return fail(NUFI_ERR_USAGE, "null argument");
+    const size_t bytes = (size_t)M * h->d * sizeof(double);
+    const double *dX = X, *dV = V;
+    double *dF = F;
+    double *tX = nullptr, *tV = nullptr, *tF = nullptr;
+    if (!is_device_ptr(X)) {
+        CU(cudaMallocAsync(&tX, bytes, h->stream));
+        CU(cudaMemcpyAsync(tX, X, bytes, cudaMemcpyHostToDevice, h->stream));
+        dX = tX;
+    }
+    if (!is_device_ptr(V)) {
+        CU(cudaMallocAsync(&tV, bytes, h->stream));
+        CU(cudaMemcpyAsync(tV, V, bytes, cudaMemcpyHostToDevice, h->stream));
+        dV = tV;
+    }
+    const bool df = is_device_ptr(F);
+    if (!df) {
+        CU(cudaMallocAsync(&tF, M * sizeof(double), h->stream));
+        dF = tF;
+    }
+    CU(launch_eval_f0(h->d, h->f0, dX, dV, M, dF, h->stream));
+    if (!df) CU(cudaMemcpyAsync(F, dF, M * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    if (tX) CU(cudaFreeAsync(tX, h->stream));
+    if (tV) CU(cudaFreeAsync(tV, h->stream));
+    if (tF) CU(cudaFreeAsync(tF, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    return NUFI_OK;
+}
+
+}  // extern "C"

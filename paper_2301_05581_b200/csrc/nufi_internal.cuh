@@ -1,0 +1,205 @@
+// nufi_internal.cuh -- device-side helpers shared by the NuFI sm_100a kernels.
+//
+// TMA bulk copies (cp.async.bulk -> SASS UBLKCP) completing on shared-memory
+// mbarriers, the magic-constant cell locator used by the production trace,
+// and the kernel parameter blocks.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "nufi.h"
+
+namespace nufi {
+
+// ----------------------------------------------------------------------------
+// constants
+// ----------------------------------------------------------------------------
+
+// 1.5 * 2^52: x + MAGIC rounds x to the nearest integer in the low mantissa bits
+// (|x| < 2^51); (x + MAGIC) - MAGIC is rint(x) and the low 32 bits of the sum's
+// bit pattern are rint(x) as a two's-complement int32.
+constexpr double MAGIC = 6755399441055744.0;
+constexpr double GAUSS_NORM = 0.3989422804014327;  // 1/sqrt(2*pi), initial.py:22
+
+constexpr int MAX_D = 3;
+constexpr int MAX_FIELD_NODES = 4096;  // single-CTA field update limit (Nx^d)
+
+// ----------------------------------------------------------------------------
+// f0 descriptor (initial.py:25-56, 165-180)
+// ----------------------------------------------------------------------------
+
+struct F0Params {
+    int d;
+    int n_centers[MAX_D];
+    int power[MAX_D];
+    double centers[MAX_D][NUFI_MAX_CENTERS];
+    double weights[MAX_D][NUFI_MAX_CENTERS];
+    double alpha;
+    double k;
+};
+
+// eval_f0 at one point (initial.py:41-49,165-180): x is NOT wrapped.
+template <int D>
+__device__ __forceinline__ double eval_f0(const F0Params &P, const double *x, const double *v) {
+    double vel = 1.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        double acc = 0.0;
+        for (int m = 0; m < P.n_centers[a]; ++m) {
+            double t = v[a] - P.centers[a][m];
+            acc += P.weights[a][m] * exp(-0.5 * (t * t));
+        }
+        acc *= GAUSS_NORM;
+        if (P.power[a]) acc = acc * (v[a] * v[a]);
+        vel = (a == 0) ? acc : vel * acc;
+    }
+    double pert = cos(P.k * x[0]);
+#pragma unroll
+    for (int a = 1; a < D; ++a) pert = pert + cos(P.k * x[a]);
+    return vel * (1.0 + P.alpha * pert);
+}
+
+// ----------------------------------------------------------------------------
+// cell location (production arithmetic)
+// ----------------------------------------------------------------------------
+
+// X is a position in cell units shifted by -1/2 (X = x*N/L - 1/2, unwrapped).
+// Returns the cell index in [0, N) and the centred offset fc in [-1/2, 1/2];
+// the reference's fraction is f = fc + 1/2 (kernels.py:153-162).
+template <bool POW2>
+__device__ __forceinline__ int locate_centred(double X, int N, double &fc) {
+    double s = X + MAGIC;
+    double r = s - MAGIC;
+    fc = X - r;
+    int ri = (int)(unsigned)(__double_as_longlong(s) & 0xffffffffull);
+    if (POW2) return ri & (N - 1);
+    int i = ri % N;
+    return i < 0 ? i + N : i;
+}
+
+// Cubic B-spline stencil weights and their t-derivatives at fraction f
+// (kernels.py:62-81 / 211-221), FMA form.
+__device__ __forceinline__ void bspline_w_dw(double f, double w[4], double dw[4]) {
+    const double s = 1.0 - f;
+    const double f2 = f * f, s2 = s * s;
+    w[0] = s2 * s * (1.0 / 6.0);
+    w[1] = fma(-f2, fma(-0.5, f, 1.0), 2.0 / 3.0);
+    w[2] = fma(-s2, fma(-0.5, s, 1.0), 2.0 / 3.0);
+    w[3] = f2 * f * (1.0 / 6.0);
+    dw[0] = -0.5 * s2;
+    dw[1] = f * fma(1.5, f, -2.0);
+    dw[2] = s * fma(-1.5, s, 2.0);
+    dw[3] = 0.5 * f2;
+}
+
+// ----------------------------------------------------------------------------
+// TMA bulk copy + mbarrier (PTX; sm_90+ incl. sm_100a)
+// ----------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// 1-D bulk copy global -> shared, completion signalled on `bar` (bytes % 16 == 0,
+// both addresses 16-byte aligned).  SASS: UBLKCP.S.G.
+__device__ __forceinline__ void tma_bulk_g2s(void *dst_smem, const void *src_gmem, uint32_t bytes,
+                                             uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst_smem)),
+        "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// ----------------------------------------------------------------------------
+// kernel parameter blocks
+// ----------------------------------------------------------------------------
+
+struct TraceRhoParams {
+    // geometry
+    int N;          // Nx
+    int nodes;      // Nx^d
+    int Nv;
+    int64_t V;      // Nv^d
+    int node_tiles; // ceil(nodes / 32)
+    int vt_rows;    // v-rows per CTA tile (warps * PPT * passes)
+    int passes;
+    int vt_lo;      // first global v-tile traced by this launch
+    // step
+    int n;          // Psi-tilde through slabs n-1 .. 0
+    // arithmetic (scaled units: X = x*inv_h - 1/2, V = v*tau*inv_h)
+    double hx, inv_h, vmax, hv;
+    double vel_to_scaled;  // tau * inv_h
+    double scaled_to_vel;  // 1 / (tau * inv_h)
+    // history of evaluation slabs (see field_update.cu for layouts)
+    const double *ev_hist;
+    int ev_slab_elems;     // doubles per evaluation slab (16-byte multiple)
+    int slabs_per_stage;
+    int stages;
+    F0Params f0;
+    // outputs: partial[vt][nodes], fminmax[vt * node_tiles + tile][2]
+    double *partial;
+    double *fminmax;
+};
+
+// per-step tail (field_update.cu)
+struct FieldParams {
+    int d, N, nodes, B;
+    double L, inv_h, hv_d, rho_bar, L_d, K;
+    double k_scale;  // 2*pi/L (poisson.py:54)
+    // inputs (one of the two)
+    const double *partials;  // [B][nodes] sums, then [B][2] (min, max)
+    const double *rho_in;    // neutral rho (nufi_field_update)
+    // step slot
+    int64_t slot;            // history row written
+    double *hist;            // (cap, nodes)
+    double *ev_hist;         // (cap, ev_slab_elems)
+    int ev_slab_elems;
+    // outputs (nullable)
+    double *rho_out;         // nodes
+    double *stats_out;       // 3: neutralization, f_min, f_max
+    double *W_out;           // 1
+    double *E_out;           // nodes * d
+    double *coeffs_out;      // nodes
+    int *status;             // set to NUFI_ERR_NUMERICAL when rho is not neutral
+    int64_t *hist_len;       // device-side history length, set to slot + 1
+    int finish_only;         // compute_rho only: stop after rho / stats
+};
+
+// background density (field_update.cu)
+struct RhoBarParams {
+    int d, N, Nv;
+    double hx, hv, vmax, hx_d, hv_d, L_d;
+    F0Params f0;
+    double *out;
+};
+
+}  // namespace nufi

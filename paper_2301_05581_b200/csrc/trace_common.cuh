@@ -1,0 +1,122 @@
+// trace_common.cuh -- one backward leapfrog substep of the NuFI characteristic trace.
+//
+// Reference semantics (kernels.py:184-387): per stored step k
+//     x -= tau * v ;  v += tau * E_k(x)        (k = n-1 .. 1)
+//     x -= tau * v ;  v += (tau/2) * E_0(x)    (last substep)
+// with E_k = -grad of the periodic cubic B-spline whose coefficients are slab k.
+//
+// Production arithmetic ("fast" mode) works in scaled units
+//     X = x * N/L - 1/2  (cell units, centred),   V = v * tau * N/L  (cells/step)
+// so a drift is one DADD and the cell lookup is the magic-constant rint of X:
+// cell i = rint(X) mod N, centred fraction fc = X - rint(X) in [-1/2, 1/2], and
+// the reference's fraction is f = fc + 1/2.  The kick scale
+//     K = -tau^2 (N/L)^2    (V += K * dphi/dt-sum, i.e. tau*N/L * tau*E)
+// is folded into the evaluation slabs (d = 1) or applied once (d = 2, 3).
+//
+// Evaluation-slab layouts (written by field_update.cu, one per stored step):
+//   d = 1: three arrays [A | B | C] of N doubles: on cell i the kick is the
+//          quadratic A_i + fc*(B_i + fc*C_i)  (the B-spline derivative restricted
+//          to one cell, pre-multiplied by K);
+//   d = 2: [N][N+3]   raw coefficients, last axis with a periodic halo
+//          (halo index j' holds c[(j'-1) mod N]) so the 4 taps are contiguous;
+//   d = 3: [N][N][N+3] same halo on the last (z) axis.
+#pragma once
+
+#include "nufi_internal.cuh"
+
+namespace nufi {
+
+__host__ __device__ constexpr int ev_slab_raw_elems(int d, int N) {
+    return d == 1 ? 3 * N : (d == 2 ? N * (N + 3) : N * N * (N + 3));
+}
+// padded to a 16-byte multiple (TMA bulk copy granularity)
+__host__ __device__ constexpr int ev_slab_elems(int d, int N) {
+    return (ev_slab_raw_elems(d, N) + 1) & ~1;
+}
+
+template <bool POW2>
+__device__ __forceinline__ int wrap_idx(int i, int N) {
+    if (POW2) return i & (N - 1);
+    i %= N;
+    return i < 0 ? i + N : i;
+}
+
+// Kick through evaluation slab `slab` (smem or global): V += K * g(X), or half of
+// it (`half`: the tau/2 kicks of kernels.py:194-196 and 203-205).
+template <int D, bool POW2>
+__device__ __forceinline__ void kick(const double (&X)[D], double (&V)[D], const double *__restrict__ slab, int N,
+                                     double K, bool half) {
+    if constexpr (D == 1) {
+        double fc;
+        const int i = locate_centred<POW2>(X[0], N, fc);
+        const double A = slab[i], B = slab[N + i], C = slab[2 * N + i];
+        const double kick = fma(fc, fma(fc, C, B), A);
+        V[0] = half ? fma(0.5, kick, V[0]) : V[0] + kick;
+        (void)K;
+    } else if constexpr (D == 2) {
+        double fx, fy;
+        const int ix = locate_centred<POW2>(X[0], N, fx);
+        const int iy = locate_centred<POW2>(X[1], N, fy);
+        double wx[4], dwx[4], wy[4], dwy[4];
+        bspline_w_dw(fx + 0.5, wx, dwx);
+        bspline_w_dw(fy + 0.5, wy, dwy);
+        const int row = N + 3;
+        double gx = 0.0, gy = 0.0;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const double *c = slab + wrap_idx<POW2>(ix - 1 + m, N) * row + iy;
+            const double c0 = c[0], c1 = c[1], c2 = c[2], c3 = c[3];
+            const double r = fma(c3, wy[3], fma(c2, wy[2], fma(c1, wy[1], c0 * wy[0])));
+            const double rd = fma(c3, dwy[3], fma(c2, dwy[2], fma(c1, dwy[1], c0 * dwy[0])));
+            gx = fma(dwx[m], r, gx);
+            gy = fma(wx[m], rd, gy);
+        }
+        const double k = half ? 0.5 * K : K;
+        V[0] = fma(k, gx, V[0]);
+        V[1] = fma(k, gy, V[1]);
+    } else {
+        double fx, fy, fz;
+        const int ix = locate_centred<POW2>(X[0], N, fx);
+        const int iy = locate_centred<POW2>(X[1], N, fy);
+        const int iz = locate_centred<POW2>(X[2], N, fz);
+        double wx[4], dwx[4], wy[4], dwy[4], wz[4], dwz[4];
+        bspline_w_dw(fx + 0.5, wx, dwx);
+        bspline_w_dw(fy + 0.5, wy, dwy);
+        bspline_w_dw(fz + 0.5, wz, dwz);
+        const int row = N + 3;
+        double gx = 0.0, gy = 0.0, gz = 0.0;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const int xm = wrap_idx<POW2>(ix - 1 + m, N) * N;
+            double sy = 0.0, sdy = 0.0, sdz = 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double *c = slab + (xm + wrap_idx<POW2>(iy - 1 + q, N)) * row + iz;
+                const double c0 = c[0], c1 = c[1], c2 = c[2], c3 = c[3];
+                const double r = fma(c3, wz[3], fma(c2, wz[2], fma(c1, wz[1], c0 * wz[0])));
+                const double rd = fma(c3, dwz[3], fma(c2, dwz[2], fma(c1, dwz[1], c0 * dwz[0])));
+                sy = fma(wy[q], r, sy);
+                sdy = fma(dwy[q], r, sdy);
+                sdz = fma(wy[q], rd, sdz);
+            }
+            gx = fma(dwx[m], sy, gx);
+            gy = fma(wx[m], sdy, gy);
+            gz = fma(wx[m], sdz, gz);
+        }
+        const double k = half ? 0.5 * K : K;
+        V[0] = fma(k, gx, V[0]);
+        V[1] = fma(k, gy, V[1]);
+        V[2] = fma(k, gz, V[2]);
+    }
+}
+
+// One backward substep: drift x -= tau v, then kick through slab.
+template <int D, bool POW2>
+__device__ __forceinline__ void substep(double (&X)[D], double (&V)[D], const double *__restrict__ slab,
+                                        int N, double K, bool half) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) X[a] -= V[a];
+    kick<D, POW2>(X, V, slab, N, K, half);
+}
+
+}  // namespace nufi

@@ -1,0 +1,248 @@
+// trace_points.cu -- kernels.trace_backward on caller-provided points, and eval_f0.
+//
+// Two arithmetic modes:
+//   FAST   the production substep of trace_common.cuh, reading the evaluation
+//          slabs from global memory (L2-resident history);
+//   PARITY the reference's exact operation sequence (kernels.py:153-387: Python
+//          float modulo via fmod + sign fix, int() truncation, weights exactly
+//          as written, contraction order m -> q -> w, no FMA contraction:
+//          __dmul_rn / __dadd_rn), reading the raw coefficient history.  It
+//          reproduces the numba kernels' X, V bit for bit.
+#include "trace_common.cuh"
+
+namespace nufi {
+
+// ---- PARITY helpers (kernels.py:153-228), no contraction ----
+#define M_(a, b) __dmul_rn((a), (b))
+#define A_(a, b) __dadd_rn((a), (b))
+#define S_(a, b) __dsub_rn((a), (b))
+
+__device__ __forceinline__ void cell_1d_exact(double x, double L, int N, double inv_h, int &i, double &f) {
+    double u = fmod(x, L);  // numba lowers Python float % to fmod + sign fix
+    if (u != 0.0) {
+        if ((L < 0.0) != (u < 0.0)) u = A_(u, L);
+    } else {
+        u = copysign(0.0, L);
+    }
+    if (u >= L || u < 0.0) u = 0.0;  // kernels.py:156-157
+    const double t = M_(u, inv_h);
+    long long ii = (long long)t;  // int(t): truncation
+    if (ii > N - 1) ii = N - 1;
+    i = (int)ii;
+    f = S_(t, (double)ii);
+}
+
+__device__ __forceinline__ void fill_weights_exact(double f, double *w, double *dw) {
+    const double s = S_(1.0, f);
+    w[0] = __ddiv_rn(M_(M_(s, s), s), 6.0);
+    w[1] = S_(2.0 / 3.0, M_(M_(f, f), S_(1.0, M_(0.5, f))));
+    w[2] = S_(2.0 / 3.0, M_(M_(s, s), S_(1.0, M_(0.5, s))));
+    w[3] = __ddiv_rn(M_(M_(f, f), f), 6.0);
+    dw[0] = M_(M_(-0.5, s), s);
+    dw[1] = M_(f, S_(M_(1.5, f), 2.0));
+    dw[2] = M_(s, S_(2.0, M_(1.5, s)));
+    dw[3] = M_(M_(0.5, f), f);
+}
+
+__device__ __forceinline__ void stencil_exact(int i, int N, int *idx) {
+    idx[0] = i > 0 ? i - 1 : N - 1;
+    idx[1] = i;
+    idx[2] = i + 1 < N ? i + 1 : i + 1 - N;
+    idx[3] = i + 2 < N ? i + 2 : i + 2 - N;
+}
+
+template <int D>
+__device__ __forceinline__ void E_exact(const double *__restrict__ c, double L, int N, double inv_h, const double *x,
+                                        double *E) {
+    if constexpr (D == 1) {  // kernels.py:164-182
+        int i;
+        double f;
+        cell_1d_exact(x[0], L, N, inv_h, i, f);
+        double w[4], dw[4];
+        fill_weights_exact(f, w, dw);
+        int idx[4];
+        stencil_exact(i, N, idx);
+        const double g = A_(A_(A_(M_(c[idx[0]], dw[0]), M_(c[idx[1]], dw[1])), M_(c[idx[2]], dw[2])),
+                            M_(c[idx[3]], dw[3]));
+        E[0] = M_(-g, inv_h);
+    } else if constexpr (D == 2) {  // kernels.py:230-249
+        int i, j;
+        double f, g;
+        double wx[4], dwx[4], wy[4], dwy[4];
+        int ix[4], iy[4];
+        cell_1d_exact(x[0], L, N, inv_h, i, f);
+        fill_weights_exact(f, wx, dwx);
+        stencil_exact(i, N, ix);
+        cell_1d_exact(x[1], L, N, inv_h, j, g);
+        fill_weights_exact(g, wy, dwy);
+        stencil_exact(j, N, iy);
+        double gx = 0.0, gy = 0.0;
+        for (int m = 0; m < 4; ++m) {
+            double r = 0.0, rd = 0.0;
+            for (int q = 0; q < 4; ++q) {
+                const double cc = c[ix[m] * N + iy[q]];
+                r = A_(r, M_(cc, wy[q]));
+                rd = A_(rd, M_(cc, dwy[q]));
+            }
+            gx = A_(gx, M_(dwx[m], r));
+            gy = A_(gy, M_(wx[m], rd));
+        }
+        E[0] = M_(-gx, inv_h);
+        E[1] = M_(-gy, inv_h);
+    } else {  // kernels.py:296-327
+        int i, j, l;
+        double f, g, h;
+        double wx[4], dwx[4], wy[4], dwy[4], wz[4], dwz[4];
+        int ix[4], iy[4], iz[4];
+        cell_1d_exact(x[0], L, N, inv_h, i, f);
+        fill_weights_exact(f, wx, dwx);
+        stencil_exact(i, N, ix);
+        cell_1d_exact(x[1], L, N, inv_h, j, g);
+        fill_weights_exact(g, wy, dwy);
+        stencil_exact(j, N, iy);
+        cell_1d_exact(x[2], L, N, inv_h, l, h);
+        fill_weights_exact(h, wz, dwz);
+        stencil_exact(l, N, iz);
+        double gx = 0.0, gy = 0.0, gz = 0.0;
+        for (int m = 0; m < 4; ++m) {
+            double sy = 0.0, sdy = 0.0, sdz = 0.0;
+            for (int q = 0; q < 4; ++q) {
+                double r = 0.0, rd = 0.0;
+                const double *row = c + (ix[m] * N + iy[q]) * N;
+                for (int w = 0; w < 4; ++w) {
+                    const double cc = row[iz[w]];
+                    r = A_(r, M_(cc, wz[w]));
+                    rd = A_(rd, M_(cc, dwz[w]));
+                }
+                sy = A_(sy, M_(wy[q], r));
+                sdy = A_(sdy, M_(dwy[q], r));
+                sdz = A_(sdz, M_(wy[q], rd));
+            }
+            gx = A_(gx, M_(dwx[m], sy));
+            gy = A_(gy, M_(wx[m], sdy));
+            gz = A_(gz, M_(wx[m], sdz));
+        }
+        E[0] = M_(-gx, inv_h);
+        E[1] = M_(-gy, inv_h);
+        E[2] = M_(-gz, inv_h);
+    }
+}
+
+// kernels.py:184-209 / 251-294 / 329-387 on the raw coefficient history.
+template <int D>
+__global__ void trace_points_parity(const double *__restrict__ hist, int N, int nodes, double L, int n, double tau,
+                                    double *X, double *V, int64_t M, int half_kick) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= M) return;
+    const double inv_h = (double)N / L;
+    const double half = M_(0.5, tau);
+    double x[D], v[D], E[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        x[a] = X[p * D + a];
+        v[a] = V[p * D + a];
+    }
+    if (half_kick) {
+        E_exact<D>(hist + (size_t)n * nodes, L, N, inv_h, x, E);
+#pragma unroll
+        for (int a = 0; a < D; ++a) v[a] = A_(v[a], M_(half, E[a]));
+    }
+    for (int k = n - 1; k >= 1; --k) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) x[a] = S_(x[a], M_(tau, v[a]));
+        E_exact<D>(hist + (size_t)k * nodes, L, N, inv_h, x, E);
+#pragma unroll
+        for (int a = 0; a < D; ++a) v[a] = A_(v[a], M_(tau, E[a]));
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a) x[a] = S_(x[a], M_(tau, v[a]));
+    E_exact<D>(hist, L, N, inv_h, x, E);
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        v[a] = A_(v[a], M_(half, E[a]));
+        X[p * D + a] = x[a];
+        V[p * D + a] = v[a];
+    }
+}
+
+#undef M_
+#undef A_
+#undef S_
+
+// Production arithmetic on caller points.  The optional leading half kick
+// (Psi, flow.py:106-112) uses slab n.
+template <int D, bool POW2>
+__global__ void trace_points_fast(const double *__restrict__ ev_hist, int ev_slab_elems, int N, double inv_h,
+                                  double tau, double K, int n, double *X, double *V, int64_t M, int half_kick) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= M) return;
+    const double s_in = tau * inv_h, s_out = 1.0 / s_in, hx = 1.0 / inv_h;
+    double Xs[D], Vs[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        Xs[a] = fma(X[p * D + a], inv_h, -0.5);
+        Vs[a] = V[p * D + a] * s_in;
+    }
+    if (half_kick && n > 0) kick<D, POW2>(Xs, Vs, ev_hist + (size_t)n * ev_slab_elems, N, K, true);
+    if (n == 0) return;
+    for (int k = n - 1; k >= 1; --k) substep<D, POW2>(Xs, Vs, ev_hist + (size_t)k * ev_slab_elems, N, K, false);
+    substep<D, POW2>(Xs, Vs, ev_hist, N, K, true);
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        X[p * D + a] = (Xs[a] + 0.5) * hx;
+        V[p * D + a] = Vs[a] * s_out;
+    }
+}
+
+template <int D>
+__global__ void eval_f0_kernel(const F0Params f0, const double *X, const double *V, int64_t M, double *F) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= M) return;
+    double x[D], v[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        x[a] = X[p * D + a];
+        v[a] = V[p * D + a];
+    }
+    F[p] = eval_f0<D>(f0, x, v);
+}
+
+cudaError_t launch_trace_points(int d, int mode, bool pow2, const double *hist, const double *ev_hist,
+                                int ev_slab_elems, int N, int nodes, double L, int n, double tau, double K, double *X,
+                                double *V, int64_t M, int half_kick, cudaStream_t st) {
+    const int threads = 128;
+    const int ctas = (int)((M + threads - 1) / threads);
+    const double inv_h = (double)N / L;
+    if (mode == NUFI_TRACE_PARITY) {
+        if (d == 1) trace_points_parity<1><<<ctas, threads, 0, st>>>(hist, N, nodes, L, n, tau, X, V, M, half_kick);
+        if (d == 2) trace_points_parity<2><<<ctas, threads, 0, st>>>(hist, N, nodes, L, n, tau, X, V, M, half_kick);
+        if (d == 3) trace_points_parity<3><<<ctas, threads, 0, st>>>(hist, N, nodes, L, n, tau, X, V, M, half_kick);
+    } else {
+#define NUFI_TP(DD)                                                                                              \
+    if (d == DD) {                                                                                               \
+        if (pow2)                                                                                                \
+            trace_points_fast<DD, true>                                                                          \
+                <<<ctas, threads, 0, st>>>(ev_hist, ev_slab_elems, N, inv_h, tau, K, n, X, V, M, half_kick);     \
+        else                                                                                                     \
+            trace_points_fast<DD, false>                                                                         \
+                <<<ctas, threads, 0, st>>>(ev_hist, ev_slab_elems, N, inv_h, tau, K, n, X, V, M, half_kick);     \
+    }
+        NUFI_TP(1)
+        NUFI_TP(2)
+        NUFI_TP(3)
+#undef NUFI_TP
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_eval_f0(int d, const F0Params &f0, const double *X, const double *V, int64_t M, double *F,
+                           cudaStream_t st) {
+    const int threads = 128;
+    const int ctas = (int)((M + threads - 1) / threads);
+    if (d == 1) eval_f0_kernel<1><<<ctas, threads, 0, st>>>(f0, X, V, M, F);
+    if (d == 2) eval_f0_kernel<2><<<ctas, threads, 0, st>>>(f0, X, V, M, F);
+    if (d == 3) eval_f0_kernel<3><<<ctas, threads, 0, st>>>(f0, X, V, M, F);
+    return cudaGetLastError();
+}
+
+}  // namespace nufi

@@ -1,0 +1,279 @@
+// trace_rho.cu -- fused Psi-tilde trace + f0 at the foot point + v-reduction.
+//
+// Replaces density.compute_rho's point loop (density.py:72-91) ->
+// flow.psi_tilde_batch (flow.py:115-121) -> kernels.trace_backward
+// (kernels.py:390-412, _trace_1d/2d/3d kernels.py:184-387) -> initial.eval_f0
+// (initial.py:165-180) -> np.add.reduce over v (density.py:80-81).
+//
+// One thread per quadrature point (x_i, v_j) with (x, v) in registers; no point
+// arrays exist (they are decoded from the thread index, unlike
+// density.py:32-42).  Warp lanes take 32 consecutive x nodes at the same v
+// (x-fastest), so the stencil gathers of neighbouring lanes hit neighbouring
+// coefficients.  The coefficient history is streamed backwards (slab n-1 first)
+// through a shared-memory ring filled by TMA bulk copies (cp.async.bulk,
+// mbarrier complete_tx) that the whole CTA shares.  The v-sum is a fixed-order
+// per-thread accumulation then a fixed-order CTA sum over warps: deterministic,
+// no atomics.
+//
+// CTA tile: 32 nodes x vt_rows v-rows (warps * PPT rows per pass).  Output:
+// partial[vt][node] (vt = global v-tile) and per-CTA (f_min, f_max).
+#include <cfloat>
+
+#include "trace_common.cuh"
+
+namespace nufi {
+
+template <int D, int PPT, bool POW2>
+__global__ void __launch_bounds__(512) trace_rho_kernel(const TraceRhoParams p, const double K) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warps = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int N = p.N;
+    const int sps = p.slabs_per_stage;
+    const int stages = p.stages;
+    const int slab_elems = p.ev_slab_elems;
+
+    double *ring = reinterpret_cast<double *>(smem_raw);
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)stages * sps * slab_elems);
+    uint64_t *empty = full + stages;
+    double *red = reinterpret_cast<double *>(empty + stages);  // 3 * blockDim.x
+
+    const int tile = blockIdx.x % p.node_tiles;
+    const int vt = p.vt_lo + blockIdx.x / p.node_tiles;
+    const int node = tile * 32 + lane;
+    const bool valid = node < p.nodes;
+
+    int ni[D];
+    {
+        int r = valid ? node : 0;
+#pragma unroll
+        for (int a = D - 1; a >= 0; --a) {
+            ni[a] = r % N;
+            r /= N;
+        }
+    }
+
+    const int n = p.n;
+    const int stages_per_pass = (n + sps - 1) / sps;
+    const int total_it = p.passes * stages_per_pass;
+
+    // Issue the bulk copy for ring iteration `it` (pass-agnostic: stage index
+    // it % stages_per_pass covers slabs [k_lo, k_hi], k_hi = n-1 - st*sps).
+    auto issue = [&](int it) {
+        const int st = it % stages_per_pass;
+        const int s = it % stages;
+        const int k_hi = n - 1 - st * sps;
+        const int k_lo = max(0, k_hi - sps + 1);
+        const uint32_t bytes = (uint32_t)((k_hi - k_lo + 1) * slab_elems * sizeof(double));
+        mbar_arrive_expect_tx(&full[s], bytes);
+        tma_bulk_g2s(ring + (size_t)s * sps * slab_elems, p.ev_hist + (size_t)k_lo * slab_elems, bytes, &full[s]);
+    };
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], warps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int it = 0; it < min(stages, total_it); ++it) issue(it);
+    }
+
+    double acc = 0.0, fmn = DBL_MAX, fmx = -DBL_MAX;
+    int it = 0;
+    for (int pass = 0; pass < p.passes; ++pass) {
+        double X[PPT][D], V[PPT][D];
+        int64_t jrow[PPT];
+#pragma unroll
+        for (int pp = 0; pp < PPT; ++pp) {
+            jrow[pp] = (int64_t)vt * p.vt_rows + (int64_t)(pass * warps + warp) * PPT + pp;
+            int64_t r = jrow[pp];
+#pragma unroll
+            for (int a = D - 1; a >= 0; --a) {
+                const int ja = (int)(r % p.Nv);
+                r /= p.Nv;
+                // grids.py:110-115: -vmax + (j + 0.5) * hv
+                const double v = __dadd_rn(-p.vmax, __dmul_rn((double)ja + 0.5, p.hv));
+                X[pp][a] = (double)ni[a] - 0.5;
+                V[pp][a] = v * p.vel_to_scaled;
+            }
+        }
+
+        for (int st = 0; st < stages_per_pass; ++st, ++it) {
+            const int s = it % stages;
+            const uint32_t u = (uint32_t)(it / stages);
+            const int k_hi = n - 1 - st * sps;
+            const int k_lo = max(0, k_hi - sps + 1);
+            mbar_wait(&full[s], u & 1u);
+            const double *buf = ring + (size_t)s * sps * slab_elems;
+            for (int k = k_hi; k >= max(k_lo, 1); --k) {
+                const double *slab = buf + (size_t)(k - k_lo) * slab_elems;
+#pragma unroll
+                for (int pp = 0; pp < PPT; ++pp) substep<D, POW2>(X[pp], V[pp], slab, N, K, false);
+            }
+            if (k_lo == 0) {
+#pragma unroll
+                for (int pp = 0; pp < PPT; ++pp) substep<D, POW2>(X[pp], V[pp], buf, N, K, true);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if (threadIdx.x == 0 && it + stages < total_it) {
+                mbar_wait(&empty[s], u & 1u);
+                issue(it + stages);
+            }
+        }
+
+#pragma unroll
+        for (int pp = 0; pp < PPT; ++pp) {
+            double x[D], v[D];
+            if (n == 0) {
+                int64_t r = jrow[pp];
+#pragma unroll
+                for (int a = D - 1; a >= 0; --a) {
+                    const int ja = (int)(r % p.Nv);
+                    r /= p.Nv;
+                    x[a] = __dmul_rn((double)ni[a], p.hx);  // grids.py:104-108
+                    v[a] = __dadd_rn(-p.vmax, __dmul_rn((double)ja + 0.5, p.hv));
+                }
+            } else {
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    x[a] = (X[pp][a] + 0.5) * p.hx;
+                    v[a] = V[pp][a] * p.scaled_to_vel;
+                }
+            }
+            const double f = eval_f0<D>(p.f0, x, v);
+            if (valid) {
+                acc += f;
+                fmn = fmin(fmn, f);
+                fmx = fmax(fmx, f);
+            }
+        }
+    }
+
+    // fixed-order CTA reduction over warps (same v-tile, same node per lane)
+    const int T = blockDim.x;
+    red[threadIdx.x] = acc;
+    red[T + threadIdx.x] = fmn;
+    red[2 * T + threadIdx.x] = fmx;
+    __syncthreads();
+    if (warp == 0) {
+        double s = 0.0, mn = DBL_MAX, mx = -DBL_MAX;
+        for (int w = 0; w < warps; ++w) {
+            s += red[w * 32 + lane];
+            mn = fmin(mn, red[T + w * 32 + lane]);
+            mx = fmax(mx, red[2 * T + w * 32 + lane]);
+        }
+        if (valid) p.partial[(size_t)vt * p.nodes + node] = s;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (lane == 0) {
+            const size_t c = (size_t)vt * p.node_tiles + tile;
+            p.fminmax[2 * c] = mn;
+            p.fminmax[2 * c + 1] = mx;
+        }
+    }
+}
+
+// partial[vt][node] -> blocks[b][node] (fixed order over the block's v-tiles);
+// per-block (min, max) after the Nx^d * B sums.  Grid: one thread per (b, node)
+// of this rank's blocks; CTA 0 additionally reduces the min / max.
+__global__ void reduce_blocks_kernel(const double *__restrict__ partial, const double *__restrict__ fminmax,
+                                     double *__restrict__ out, int nodes, int node_tiles, int vt_per_block,
+                                     int b_lo, int b_hi, int B) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t count = (int64_t)(b_hi - b_lo) * nodes;
+    if (tid < count) {
+        const int b = b_lo + (int)(tid / nodes);
+        const int node = (int)(tid % nodes);
+        const double *src = partial + (size_t)b * vt_per_block * nodes + node;
+        double s = 0.0;
+        for (int t = 0; t < vt_per_block; ++t) s += src[(size_t)t * nodes];
+        out[(size_t)b * nodes + node] = s;
+    }
+    if (blockIdx.x == 0) {
+        double *mm = out + (size_t)B * nodes;
+        for (int b = b_lo; b < b_hi; ++b) {
+            double mn = DBL_MAX, mx = -DBL_MAX;
+            const int64_t c0 = (int64_t)b * vt_per_block * node_tiles;
+            const int64_t c1 = c0 + (int64_t)vt_per_block * node_tiles;
+            for (int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+                mn = fmin(mn, fminmax[2 * c]);
+                mx = fmax(mx, fminmax[2 * c + 1]);
+            }
+            __shared__ double smn[32], smx[32];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            }
+            if ((threadIdx.x & 31) == 0) {
+                smn[threadIdx.x >> 5] = mn;
+                smx[threadIdx.x >> 5] = mx;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+                    mn = fmin(mn, smn[w]);
+                    mx = fmax(mx, smx[w]);
+                }
+                mm[2 * b] = mn;
+                mm[2 * b + 1] = mx;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------
+// host-side launch helpers
+// ----------------------------------------------------------------------------
+
+size_t trace_rho_smem_bytes(const TraceRhoParams &p, int threads) {
+    return (size_t)p.stages * p.slabs_per_stage * p.ev_slab_elems * sizeof(double) +
+           2 * p.stages * sizeof(uint64_t) + 3 * (size_t)threads * sizeof(double);
+}
+
+template <int D, int PPT, bool POW2>
+static cudaError_t launch_one(const TraceRhoParams &p, double K, int ctas, int threads, size_t smem,
+                              cudaStream_t st) {
+    auto kern = trace_rho_kernel<D, PPT, POW2>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<ctas, threads, smem, st>>>(p, K);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_trace_rho(int d, int ppt, bool pow2, const TraceRhoParams &p, double K, int ctas, int threads,
+                             cudaStream_t st) {
+    const size_t smem = trace_rho_smem_bytes(p, threads);
+#define NUFI_TR(DD, PP)                                                                              \
+    if (d == DD && ppt == PP)                                                                        \
+        return pow2 ? launch_one<DD, PP, true>(p, K, ctas, threads, smem, st)                        \
+                    : launch_one<DD, PP, false>(p, K, ctas, threads, smem, st);
+    NUFI_TR(1, 1)
+    NUFI_TR(2, 1)
+    NUFI_TR(3, 1)
+    NUFI_TR(2, 2)
+    NUFI_TR(3, 2)
+#undef NUFI_TR
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_reduce_blocks(const double *partial, const double *fminmax, double *out, int nodes,
+                                 int node_tiles, int vt_per_block, int b_lo, int b_hi, int B, cudaStream_t st) {
+    const int64_t count = (int64_t)(b_hi - b_lo) * nodes;
+    const int threads = 256;
+    const int ctas = (int)std::max<int64_t>(1, (count + threads - 1) / threads);
+    reduce_blocks_kernel<<<ctas, threads, 0, st>>>(partial, fminmax, out, nodes, node_tiles, vt_per_block, b_lo,
+                                                   b_hi, B);
+    return cudaGetLastError();
+}
+
+}  // namespace nufi
