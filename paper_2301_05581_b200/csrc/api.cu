@@ -13,7 +13,7 @@
 #include <string>
 #include <vector>
 
-#include "trace_common.cuh"
+#include "field_common.cuh"
 
 namespace nufi {
 size_t trace_rho_smem_bytes(const TraceRhoParams &p, int threads);
@@ -26,6 +26,21 @@ cudaError_t launch_trace_points(int d, int mode, bool pow2, const double *hist, 
                                 double *V, int64_t M, int half_kick, cudaStream_t st);
 cudaError_t launch_eval_f0(int d, const F0Params &f0, const double *X, const double *V, int64_t M, double *F,
                            cudaStream_t st);
+cudaError_t launch_trace_rho_1d(const TraceRhoParams &p, const FieldParams &fp, int fuse, unsigned *ticket, int ctas,
+                                int threads, cudaStream_t st);
+int trace_rho_1d_sps(int N);
+cudaError_t launch_field_tables(double *tw, double *fac, double *k2, int d, int N, int nodes, double k_scale,
+                                cudaStream_t st);
+struct Run1DParams {
+    TraceRhoParams tp;
+    FieldParams fp;
+    int n_first, n_last;
+    double *rho_hist, *E_hist, *W_hist, *stats_hist;
+    unsigned *barrier;
+    int tiles;
+    unsigned long long *stamps;
+};
+cudaError_t launch_run_1d(const Run1DParams &P, int threads, int device, cudaStream_t st, int *grid_out);
 cudaError_t launch_build_ev_slabs(const double *hist, double *ev_hist, int d, int N, int nodes, int ev_slab_elems,
                                   double K, int64_t r0, int64_t r1, cudaStream_t st);
 }  // namespace nufi
@@ -87,6 +102,9 @@ struct nufi_handle {
     double *hist = nullptr, *ev_hist = nullptr;
     double *partial = nullptr, *fminmax = nullptr, *blocks = nullptr;
     double *d_rho = nullptr, *d_E = nullptr, *d_W = nullptr, *d_stats = nullptr, *d_rho_bar = nullptr;
+    double *tables = nullptr;  // field_common.cuh constant tables: 4N + 3 Nx^d doubles
+    unsigned *ticket = nullptr;  // last-CTA-done counter of the fused d = 1 step
+    unsigned *barrier = nullptr;  // grid-barrier counter of the persistent d = 1 run kernel
     int *d_status = nullptr;
     int64_t *d_len = nullptr;
     // run outputs (device) and their pinned host staging
@@ -206,7 +224,7 @@ static void choose_tiling(nufi_handle *h) {
     const int64_t per_block = h->V / h->B;
     int warps, ppt, passes;
     if (h->d == 1) {
-        warps = 4, ppt = 1, passes = 1;
+        warps = 8, ppt = 1, passes = 1;  // trace_rho_1d: one point per thread
     } else if (h->d == 2) {
         warps = 8, ppt = 1, passes = 1;
     } else {
@@ -226,8 +244,9 @@ static void choose_tiling(nufi_handle *h) {
     // TMA ring: slabs per stage and stage count
     const int slab_bytes = h->ev_elems * 8;
     if (h->d == 1) {
-        h->sps = std::max(1, std::min(16, 24576 / slab_bytes));
-        h->stages = 3;
+        h->sps = trace_rho_1d_sps(h->N);  // must match the kernel's template instantiation
+        h->stages = h->N >= 256 ? 2 : 4;  // 2 CTAs / SM for the large-N (throughput-bound) case
+        if (const char *e = getenv("NUFI_D1_STAGES")) h->stages = std::max(2, atoi(e));
     } else if (h->d == 2) {
         h->sps = std::max(1, 16384 / slab_bytes);
         h->stages = 3;
@@ -363,6 +382,10 @@ int nufi_create(const nufi_config *cfg, int device, void *stream, nufi_handle **
     h->K = -(c.tau * c.tau) * (h->inv_h * h->inv_h);
     // v-blocks (fixed combine order, independent of the rank count)
     int B = c.v_blocks > 0 ? c.v_blocks : 8;
+    if (B > 8) {
+        delete h;
+        return fail(NUFI_ERR_USAGE, "v_blocks must be <= 8");
+    }
     while (B > 1 && (h->V % B != 0)) --B;
     if (c.v_blocks > 0 && B != c.v_blocks) {
         delete h;
@@ -391,6 +414,12 @@ int nufi_create(const nufi_config *cfg, int device, void *stream, nufi_handle **
     CU(cudaMalloc(&h->d_rho_bar, sizeof(double)));
     CU(cudaMalloc(&h->d_status, sizeof(int)));
     CU(cudaMalloc(&h->d_len, sizeof(int64_t)));
+    CU(cudaMalloc(&h->tables, (4 * (size_t)h->N + 3 * nodes) * sizeof(double)));
+    CU(cudaMalloc(&h->ticket, sizeof(unsigned)));
+    CU(cudaMalloc(&h->barrier, sizeof(unsigned)));
+    CU(cudaMemsetAsync(h->ticket, 0, sizeof(unsigned), h->stream));
+    CU(launch_field_tables(h->tables, h->tables + 2 * h->N, h->tables + 2 * h->N + 2 * nodes, c.d, c.Nx, h->nodes,
+                           2.0 * M_PI / c.L, h->stream));
     CU(cudaMemsetAsync(h->d_status, 0, sizeof(int), h->stream));
     CU(cudaMemsetAsync(h->d_len, 0, sizeof(int64_t), h->stream));
 
@@ -409,7 +438,8 @@ int nufi_destroy(nufi_handle *h) {
     cudaStreamSynchronize(h->stream);
     for (void *p : {(void *)h->hist, (void *)h->ev_hist, (void *)h->partial, (void *)h->fminmax, (void *)h->blocks,
                     (void *)h->d_rho, (void *)h->d_E, (void *)h->d_W, (void *)h->d_stats, (void *)h->d_rho_bar,
-                    (void *)h->d_status, (void *)h->d_len, (void *)h->run_dev})
+                    (void *)h->d_status, (void *)h->d_len, (void *)h->run_dev, (void *)h->tables,
+                    (void *)h->ticket, (void *)h->barrier})
         if (p) cudaFree(p);
     if (h->run_host) cudaFreeHost(h->run_host);
     if (h->own_stream) cudaStreamDestroy(h->stream);
@@ -488,9 +518,7 @@ int nufi_truncate_history(nufi_handle *h, int64_t count) {
 
 // ---- internal step pieces -------------------------------------------------
 
-// trace + per-tile sums for blocks [b_lo, b_hi) -> out (B*nodes sums + 2B min/max)
-static int enqueue_partials(nufi_handle *h, int64_t n, int b_lo, int b_hi, double *out) {
-    if (b_hi <= b_lo) return NUFI_OK;
+static TraceRhoParams trace_params(nufi_handle *h, int64_t n, int b_lo) {
     TraceRhoParams p{};
     p.N = h->N;
     p.nodes = h->nodes;
@@ -514,17 +542,7 @@ static int enqueue_partials(nufi_handle *h, int64_t n, int b_lo, int b_hi, doubl
     p.f0 = h->f0;
     p.partial = h->partial;
     p.fminmax = h->fminmax;
-    const int ctas = (b_hi - b_lo) * h->vt_per_block * h->node_tiles;
-    {
-        ProfScope ps(h, 0, (double)h->nodes * (double)(h->V / h->B) * (b_hi - b_lo) * (double)n);
-        CU(launch_trace_rho(h->d, h->ppt, h->pow2, p, h->K, ctas, h->threads, h->stream));
-    }
-    {
-        ProfScope ps(h, 1);
-        CU(launch_reduce_blocks(h->partial, h->fminmax, out, h->nodes, h->node_tiles, h->vt_per_block, b_lo, b_hi,
-                                h->B, h->stream));
-    }
-    return NUFI_OK;
+    return p;
 }
 
 static FieldParams field_params(nufi_handle *h) {
@@ -539,13 +557,86 @@ static FieldParams field_params(nufi_handle *h) {
     f.rho_bar = h->rho_bar;
     f.L_d = h->L_d;
     f.K = h->K;
-    f.k_scale = 2.0 * M_PI / h->cfg.L;
+    f.twc = h->tables;
+    f.tws = h->tables + h->N;
+    f.fac = h->tables + 2 * h->N;
+    f.k2 = h->tables + 2 * h->N + 2 * h->nodes;
+    if (h->d == 1) {
+        f.gc = f.k2 + h->nodes;
+        f.gp = f.gc + h->N;
+    }
     f.hist = h->hist;
     f.ev_hist = h->ev_hist;
     f.ev_slab_elems = h->ev_elems;
     f.status = h->d_status;
     f.hist_len = h->d_len;
     return f;
+}
+
+static double point_steps(nufi_handle *h, int64_t n, int nblocks) {
+    return (double)h->nodes * (double)(h->V / h->B) * nblocks * (double)n;
+}
+
+// trace + f0 + per-tile v-sums for blocks [b_lo, b_hi) (no tail)
+static int enqueue_trace(nufi_handle *h, int64_t n, int b_lo, int b_hi) {
+    const TraceRhoParams p = trace_params(h, n, b_lo);
+    const int ctas = (b_hi - b_lo) * h->vt_per_block * h->node_tiles;
+    ProfScope ps(h, 0, point_steps(h, n, b_hi - b_lo));
+    if (h->d == 1) {
+        FieldParams none{};
+        CU(launch_trace_rho_1d(p, none, 0, h->ticket, ctas, h->threads + 32, h->stream));
+    } else {
+        CU(launch_trace_rho(h->d, h->ppt, h->pow2, p, h->K, ctas, h->threads, h->stream));
+    }
+    return NUFI_OK;
+}
+
+// per-tile sums -> block table rows [b_lo, b_hi) of out (B*nodes sums, then B (min, max))
+static int enqueue_reduce(nufi_handle *h, int b_lo, int b_hi, double *out) {
+    ProfScope ps(h, 1);
+    CU(launch_reduce_blocks(h->partial, h->fminmax, out, h->nodes, h->node_tiles, h->vt_per_block, b_lo, b_hi, h->B,
+                            h->stream));
+    return NUFI_OK;
+}
+
+// outputs of one step (device pointers, any may be null)
+struct StepOut {
+    double *rho = nullptr, *E = nullptr, *W = nullptr, *stats = nullptr;
+};
+
+// A whole single-rank step n: compute_rho (+ the field update tail when full).
+// d = 1: one fused launch (the last CTA runs the tail); d = 2, 3: trace ->
+// block reduce -> field_update.
+static int enqueue_step(nufi_handle *h, int64_t n, bool full, const StepOut &o) {
+    FieldParams f = field_params(h);
+    f.slot = n;
+    f.rho_out = o.rho;
+    f.stats_out = o.stats;
+    f.W_out = o.W;
+    f.E_out = o.E;
+    f.finish_only = full ? 0 : 1;
+    static const bool nofuse = getenv("NUFI_NOFUSE") != nullptr;
+    if (h->d == 1 && !nofuse) {
+        f.sums = h->partial;
+        f.rows_per_block = h->vt_per_block;
+        f.minmax = h->fminmax;
+        f.mm_per_block = h->vt_per_block * h->node_tiles;
+        const TraceRhoParams p = trace_params(h, n, 0);
+        const int ctas = h->B * h->vt_per_block * h->node_tiles;
+        ProfScope ps(h, 0, point_steps(h, n, h->B));
+        CU(launch_trace_rho_1d(p, f, 1, h->ticket, ctas, h->threads + 32, h->stream));
+        return NUFI_OK;
+    }
+    int rc = enqueue_trace(h, n, 0, h->B);
+    if (!rc) rc = enqueue_reduce(h, 0, h->B, h->blocks);
+    if (rc) return rc;
+    f.sums = h->blocks;
+    f.rows_per_block = 1;
+    f.minmax = h->blocks + (size_t)h->B * h->nodes;
+    f.mm_per_block = 1;
+    ProfScope ps(h, 2);
+    CU(launch_field_update(f, h->stream));
+    return NUFI_OK;
 }
 
 static int copy_out(nufi_handle *h, void *dst, const void *src, size_t bytes) {
@@ -566,22 +657,35 @@ static int check_status(nufi_handle *h, const char *what) {
     return NUFI_OK;
 }
 
+static int usage_history(nufi_handle *h, int64_t n) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "psi_tilde at step %lld needs fields 0..%lld; history holds %lld", (long long)n,
+             (long long)(n - 1), (long long)h->len);  // flow.py:55-62
+    return fail(NUFI_ERR_USAGE, buf);
+}
+
+static int copy_step_outputs(nufi_handle *h, double *rho_out, double *E_out, double *W_out, double *stats3) {
+    int rc = copy_out(h, rho_out, h->d_rho, h->nodes * sizeof(double));
+    if (!rc) rc = copy_out(h, E_out, h->d_E, (size_t)h->nodes * h->d * sizeof(double));
+    if (!rc) rc = copy_out(h, W_out, h->d_W, sizeof(double));
+    if (!rc) rc = copy_out(h, stats3, h->d_stats, 3 * sizeof(double));
+    if (rc) return rc;
+    CU(cudaStreamSynchronize(h->stream));
+    return NUFI_OK;
+}
+
 extern "C" {
 
 int nufi_rho_partials(nufi_handle *h, int64_t n, double *partials, int64_t *evals) {
     CHECK_HANDLE(h);
     if (n < 0) return fail(NUFI_ERR_USAGE, "step index must be >= 0");
-    if (n > 0 && h->len < n) {
-        char buf[160];
-        snprintf(buf, sizeof buf, "psi_tilde at step %lld needs fields 0..%lld; history holds %lld", (long long)n,
-                 (long long)(n - 1), (long long)h->len);  // flow.py:55-62
-        return fail(NUFI_ERR_USAGE, buf);
-    }
+    if (n > 0 && h->len < n) return usage_history(h, n);
     if (!is_device_ptr(partials)) return fail(NUFI_ERR_USAGE, "partials must be a device buffer");
     CU(cudaMemsetAsync(partials, 0, nufi_partials_len(h) * sizeof(double), h->stream));
-    int rc = enqueue_partials(h, n, h->b_lo, h->b_hi, partials);
+    int rc = enqueue_trace(h, n, h->b_lo, h->b_hi);
+    if (!rc) rc = enqueue_reduce(h, h->b_lo, h->b_hi, partials);
     if (rc) return rc;
-    if (evals) *evals += (int64_t)h->nodes * (h->V / h->B) * (h->b_hi - h->b_lo) * n;
+    if (evals) *evals += (int64_t)point_steps(h, n, h->b_hi - h->b_lo);
     return NUFI_OK;
 }
 
@@ -589,7 +693,10 @@ int nufi_rho_finish(nufi_handle *h, const double *partials, double *rho_out, dou
     CHECK_HANDLE(h);
     if (!is_device_ptr(partials)) return fail(NUFI_ERR_USAGE, "partials must be a device buffer");
     FieldParams f = field_params(h);
-    f.partials = partials;
+    f.sums = partials;
+    f.rows_per_block = 1;
+    f.minmax = partials + (size_t)h->B * h->nodes;
+    f.mm_per_block = 1;
     f.rho_out = h->d_rho;
     f.stats_out = h->d_stats;
     f.finish_only = 1;
@@ -597,26 +704,20 @@ int nufi_rho_finish(nufi_handle *h, const double *partials, double *rho_out, dou
         ProfScope ps(h, 2);
         CU(launch_field_update(f, h->stream));
     }
-    int rc = copy_out(h, rho_out, h->d_rho, h->nodes * sizeof(double));
-    if (!rc) rc = copy_out(h, stats3, h->d_stats, 3 * sizeof(double));
-    if (rc) return rc;
-    CU(cudaStreamSynchronize(h->stream));
-    return NUFI_OK;
+    return copy_step_outputs(h, rho_out, nullptr, nullptr, stats3);
 }
 
 int nufi_rho(nufi_handle *h, int64_t n, double *rho_out, double *stats3, int64_t *evals) {
     CHECK_HANDLE(h);
     if (n < 0) return fail(NUFI_ERR_USAGE, "step index must be >= 0");
-    if (n > 0 && h->len < n) {
-        char buf[160];
-        snprintf(buf, sizeof buf, "psi_tilde at step %lld needs fields 0..%lld; history holds %lld", (long long)n,
-                 (long long)(n - 1), (long long)h->len);
-        return fail(NUFI_ERR_USAGE, buf);
-    }
-    int rc = enqueue_partials(h, n, 0, h->B, h->blocks);
+    if (n > 0 && h->len < n) return usage_history(h, n);
+    StepOut o;
+    o.rho = h->d_rho;
+    o.stats = h->d_stats;
+    int rc = enqueue_step(h, n, false, o);
     if (rc) return rc;
-    if (evals) *evals += (int64_t)h->nodes * h->V * n;
-    return nufi_rho_finish(h, h->blocks, rho_out, stats3);
+    if (evals) *evals += (int64_t)point_steps(h, n, h->B);
+    return copy_step_outputs(h, rho_out, nullptr, nullptr, stats3);
 }
 
 int nufi_field_update(nufi_handle *h, const double *rho, double *W_out, double *E_out, double *coeffs_out) {
@@ -636,12 +737,9 @@ int nufi_field_update(nufi_handle *h, const double *rho, double *W_out, double *
     int rc = check_status(h, "solve_poisson");
     if (rc) return rc;
     h->len += 1;
-    rc = copy_out(h, W_out, h->d_W, sizeof(double));
-    if (!rc) rc = copy_out(h, E_out, h->d_E, (size_t)h->nodes * h->d * sizeof(double));
-    if (!rc) rc = copy_out(h, coeffs_out, h->hist + (size_t)(h->len - 1) * h->nodes, h->nodes * sizeof(double));
+    rc = copy_out(h, coeffs_out, h->hist + (size_t)(h->len - 1) * h->nodes, h->nodes * sizeof(double));
     if (rc) return rc;
-    CU(cudaStreamSynchronize(h->stream));
-    return NUFI_OK;
+    return copy_step_outputs(h, nullptr, E_out, W_out, nullptr);
 }
 
 int nufi_step(nufi_handle *h, int64_t n, double *rho_out, double *E_out, double *W_out, double *stats3,
@@ -654,30 +752,17 @@ int nufi_step(nufi_handle *h, int64_t n, double *rho_out, double *E_out, double 
         return fail(NUFI_ERR_USAGE, buf);
     }
     if (n >= h->cap) return fail(NUFI_ERR_USAGE, "history is full (capacity n_max + 1)");
-    int rc = enqueue_partials(h, n, 0, h->B, h->blocks);
-    if (rc) return rc;
-    FieldParams f = field_params(h);
-    f.partials = h->blocks;
-    f.slot = n;
-    f.rho_out = h->d_rho;
-    f.stats_out = h->d_stats;
-    f.W_out = h->d_W;
-    f.E_out = h->d_E;
-    {
-        ProfScope ps(h, 2);
-        CU(launch_field_update(f, h->stream));
-    }
-    rc = check_status(h, "solve_poisson");
+    StepOut o;
+    o.rho = h->d_rho;
+    o.E = h->d_E;
+    o.W = h->d_W;
+    o.stats = h->d_stats;
+    int rc = enqueue_step(h, n, true, o);
+    if (!rc) rc = check_status(h, "solve_poisson");
     if (rc) return rc;
     h->len += 1;
-    if (evals) *evals += (int64_t)h->nodes * h->V * n;
-    rc = copy_out(h, rho_out, h->d_rho, h->nodes * sizeof(double));
-    if (!rc) rc = copy_out(h, E_out, h->d_E, (size_t)h->nodes * h->d * sizeof(double));
-    if (!rc) rc = copy_out(h, W_out, h->d_W, sizeof(double));
-    if (!rc) rc = copy_out(h, stats3, h->d_stats, 3 * sizeof(double));
-    if (rc) return rc;
-    CU(cudaStreamSynchronize(h->stream));
-    return NUFI_OK;
+    if (evals) *evals += (int64_t)point_steps(h, n, h->B);
+    return copy_step_outputs(h, rho_out, E_out, W_out, stats3);
 }
 
 int nufi_step_finish(nufi_handle *h, int64_t n, const double *partials, double *rho_out, double *E_out,
@@ -687,7 +772,10 @@ int nufi_step_finish(nufi_handle *h, int64_t n, const double *partials, double *
     if (n >= h->cap) return fail(NUFI_ERR_USAGE, "history is full (capacity n_max + 1)");
     if (!is_device_ptr(partials)) return fail(NUFI_ERR_USAGE, "partials must be a device buffer");
     FieldParams f = field_params(h);
-    f.partials = partials;
+    f.sums = partials;
+    f.rows_per_block = 1;
+    f.minmax = partials + (size_t)h->B * h->nodes;
+    f.mm_per_block = 1;
     f.slot = n;
     f.rho_out = h->d_rho;
     f.stats_out = h->d_stats;
@@ -700,13 +788,7 @@ int nufi_step_finish(nufi_handle *h, int64_t n, const double *partials, double *
     int rc = check_status(h, "solve_poisson");
     if (rc) return rc;
     h->len += 1;
-    rc = copy_out(h, rho_out, h->d_rho, h->nodes * sizeof(double));
-    if (!rc) rc = copy_out(h, E_out, h->d_E, (size_t)h->nodes * h->d * sizeof(double));
-    if (!rc) rc = copy_out(h, W_out, h->d_W, sizeof(double));
-    if (!rc) rc = copy_out(h, stats3, h->d_stats, 3 * sizeof(double));
-    if (rc) return rc;
-    CU(cudaStreamSynchronize(h->stream));
-    return NUFI_OK;
+    return copy_step_outputs(h, rho_out, E_out, W_out, stats3);
 }
 
 int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, double *W_hist, double *stats_hist,
@@ -740,26 +822,82 @@ int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, d
     for (int q = 0; q < 4; ++q)
         if (dev[q]) base_dev[q] = user[q];
 
+    static const bool nopersist = getenv("NUFI_NOPERSIST") != nullptr;
+    if (h->d == 1 && !nopersist) {
+        // whole run in one cooperative launch (run_1d.cu)
+        Run1DParams P{};
+        P.tp = trace_params(h, 0, 0);
+        P.fp = field_params(h);
+        P.fp.sums = h->partial;
+        P.fp.rows_per_block = h->vt_per_block;
+        P.fp.minmax = h->fminmax;
+        P.fp.mm_per_block = h->vt_per_block * h->node_tiles;
+        P.n_first = (int)first;
+        P.n_last = (int)n_last;
+        P.rho_hist = base_dev[0];
+        P.E_hist = base_dev[1];
+        P.W_hist = base_dev[2];
+        P.stats_hist = base_dev[3];
+        P.barrier = h->barrier;
+        P.tiles = h->B * h->vt_per_block * h->node_tiles;
+        static const char *stamp_path = getenv("NUFI_STAMPS");  // debug: per-step phase timestamps
+        unsigned long long *stamps = nullptr;
+        if (stamp_path) CU(cudaMalloc(&stamps, (3 * steps + 10 + 6 * 1024) * sizeof(unsigned long long)));
+        if (stamps) CU(cudaMemsetAsync(stamps, 0, (3 * steps + 10 + 6 * 1024) * sizeof(unsigned long long), h->stream));
+        P.stamps = stamps;
+        CU(cudaMemsetAsync(h->barrier, 0, sizeof(unsigned), h->stream));
+        {
+            const double ps = (double)h->nodes * h->V * (double)((n_last * (n_last + 1) - (first - 1) * first) / 2);
+            ProfScope prof(h, 0, ps);
+            int grid = 0;
+            CU(launch_run_1d(P, h->threads + 32, h->device, h->stream, &grid));
+        }
+        if (stamps) {
+            std::vector<unsigned long long> st(3 * steps + 10 + 6 * 1024);
+            CU(cudaMemcpyAsync(st.data(), stamps, st.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                               h->stream));
+            CU(cudaStreamSynchronize(h->stream));
+            cudaFree(stamps);
+            if (FILE *f = fopen(stamp_path, "w")) {
+                for (int64_t i = 0; i < steps; ++i)
+                    fprintf(f, "%lld %llu %llu %llu\n", (long long)(first + i), st[3 * i], st[3 * i + 1], st[3 * i + 2]);
+                fprintf(f, "# tail phases (last step):");
+                for (int k = 0; k < 9; ++k) fprintf(f, " %llu", st[3 * steps + k]);
+                fprintf(f, "\n");
+                fprintf(f, "# wait/total cycles per cta (last step):");
+                for (int c = 0; c < 1024; ++c)
+                    if (st[3 * steps + 10 + 4 * 1024 + 2 * c + 1])
+                        fprintf(f, " %llu/%llu", st[3 * steps + 10 + 4 * 1024 + 2 * c], st[3 * steps + 10 + 4 * 1024 + 2 * c + 1]);
+                fprintf(f, "\n");
+                for (int q = 0; q < 4; ++q) {
+                    fprintf(f, "# cta trace end, step %d:", 400 * (q + 1));
+                    for (int c = 0; c < 1024; ++c)
+                        if (st[3 * steps + 10 + q * 1024 + c]) fprintf(f, " %llu", st[3 * steps + 10 + q * 1024 + c]);
+                    fprintf(f, "\n");
+                }
+                fclose(f);
+            }
+        }
+        for (int q = 0; q < 4; ++q)
+            if (user[q] && !dev[q])
+                CU(cudaMemcpyAsync(base_host[q], base_dev[q], steps * width[q] * sizeof(double),
+                                   cudaMemcpyDeviceToHost, h->stream));
+    } else {
     for (int64_t n = first; n <= n_last; ++n) {
         const int64_t row = n - first;
-        int rc = enqueue_partials(h, n, 0, h->B, h->blocks);
+        StepOut o;
+        o.rho = base_dev[0] + row * width[0];
+        o.E = base_dev[1] + row * width[1];
+        o.W = base_dev[2] + row * width[2];
+        o.stats = base_dev[3] + row * width[3];
+        int rc = enqueue_step(h, n, true, o);
         if (rc) return rc;
-        FieldParams f = field_params(h);
-        f.partials = h->blocks;
-        f.slot = n;
-        f.rho_out = base_dev[0] + row * width[0];
-        f.E_out = base_dev[1] + row * width[1];
-        f.W_out = base_dev[2] + row * width[2];
-        f.stats_out = base_dev[3] + row * width[3];
-        {
-        ProfScope ps(h, 2);
-        CU(launch_field_update(f, h->stream));
-    }
         // per-step device -> pinned host copies of host-bound outputs (async)
         for (int q = 0; q < 4; ++q)
             if (user[q] && !dev[q])
                 CU(cudaMemcpyAsync(base_host[q] + row * width[q], base_dev[q] + row * width[q],
                                    width[q] * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    }
     }
     int rc = check_status(h, "solve_poisson");  // synchronises
     if (rc) return rc;

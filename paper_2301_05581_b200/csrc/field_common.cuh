@@ -1,0 +1,531 @@
+// field_common.cuh -- the per-step tail of the NuFI loop as a CTA-wide device routine.
+//
+// Replaces, per step:
+//   density.compute_rho's combine + neutralisation   density.py:80-85
+//   poisson.solve_poisson                             poisson.py:90-112
+//   spline.fit_spline                                 spline.py:71-86
+//   PotentialHistory.append                           spline.py:132-142
+//   poisson.electric_energy                           poisson.py:115-120
+//   E at the nodes (SplineField.eval_E_many)          spline.py:50-52, kernels.py:102-123
+//
+// Spectral steps are separable shared-memory DFTs (Nx^d <= 4096) with exact
+// integer twiddle indices; every output's sum is split over G lanes and
+// combined with warp shuffles, so one CTA finishes a 64-point problem in ~1 us.
+// fit_spline's forward FFT of phi is fused away: for real rho the spectrum of
+// phi is phi_hat * N^d, so the coefficient slab is Re IDFT(phi_hat / prod sym)
+// (poisson.py:85-87 then spline.py:78-84, one transform pair instead of two).
+// The constant per-mode factors 1 / (N^d k^2 prod_a sym(alpha_a)) and k^2 are
+// tabulated once per handle (field_tables_kernel).
+//
+// Called by field_update_kernel (one CTA) and, for d = 1, by the last CTA of
+// the fused trace kernel (trace_rho_1d.cu) so a whole step is one launch.
+#pragma once
+
+#include <cfloat>
+
+#include "trace_common.cuh"
+
+namespace nufi {
+
+struct FieldParams {
+    int d, N, nodes, B;
+    double L, inv_h, hv_d, rho_bar, L_d;
+    double K;  // kick scale of the evaluation slabs (trace_common.cuh)
+    // constant tables (device, field_tables_kernel): twiddles cos/sin(2 pi m / N);
+    // fac[0:nodes] = 1 / (N^d k^2 prod_a sym(alpha_a)) (0 at the zero / Nyquist modes),
+    // fac[nodes:2 nodes] = prod_a sym(alpha_a); k2 = |2 pi alpha / L|^2
+    const double *twc, *tws, *fac, *k2;
+    // d = 1 only: circulant kernels of the (linear, translation-invariant) field
+    // map, c = gc (*) rho and phi = gp (*) rho (field_conv_kernels_kernel)
+    const double *gc, *gp;
+    // v-sums: B blocks of rows_per_block rows of Nx^d sums, combined in fixed order;
+    // min / max: B blocks of mm_per_block (min, max) pairs
+    const double *sums;
+    int rows_per_block;
+    const double *minmax;
+    int mm_per_block;
+    const double *rho_in;  // alternative input: a neutral rho (nufi_field_update)
+    // step slot
+    int64_t slot;
+    double *hist;     // (cap, nodes) raw coefficient history
+    double *ev_hist;  // (cap, ev_slab_elems) evaluation slabs
+    int ev_slab_elems;
+    // outputs (nullable)
+    double *rho_out, *stats_out, *W_out, *E_out, *coeffs_out;
+    double *ev_local;   // optional second destination of the evaluation slab (persistent kernel smem)
+    int *status;        // NUFI_ERR_NUMERICAL when rho is not neutral
+    int64_t *hist_len;  // device-side history length (slot + 1)
+    int finish_only;    // compute_rho only: stop after rho / stats
+    unsigned long long *tstamps;  // debug: phase timestamps (thread 0), 10 slots
+};
+
+#define NUFI_STAMP(p, k)                                                              \
+    do {                                                                              \
+        if ((p).tstamps && threadIdx.x == 0) {                                        \
+            unsigned long long _t;                                                    \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                   \
+            (p).tstamps[k] = _t;                                                      \
+        }                                                                             \
+    } while (0)
+
+// shared-memory doubles the routine needs: 4 work arrays, twiddles, the
+// per-block sums (B <= 8 blocks staged when rows_per_block > 1), scratch
+__host__ __device__ constexpr int field_smem_doubles(int nodes, int N, bool staged) {
+    return 4 * nodes + 2 * N + (staged ? 8 * nodes : 0) + 64;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// CTA-wide sum in a fixed order (deterministic for a fixed blockDim).
+__device__ __forceinline__ double cta_sum(double v, double *scratch) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) scratch[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += scratch[w];
+    __syncthreads();
+    return s;
+}
+
+__device__ __forceinline__ double cta_max(double v, double *scratch) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if (lane == 0) scratch[warp] = v;
+    __syncthreads();
+    double s = -DBL_MAX;
+    for (int w = 0; w < nw; ++w) s = fmax(s, scratch[w]);
+    __syncthreads();
+    return s;
+}
+
+// One separable DFT pass along the axis of stride st:
+//   out[e] = sum_x in[e with x on the axis] * exp(sign * 2 pi i alpha x / N)
+// Each output is summed by G consecutive lanes (G | 32), combined by shuffles.
+__device__ __forceinline__ void dft_pass(const double *__restrict__ ire, const double *__restrict__ iim,
+                                         double *__restrict__ ore, double *__restrict__ oim,
+                                         const double *__restrict__ twc, const double *__restrict__ tws, int N,
+                                         int nodes, int st, double sign, int G, bool pow2) {
+    const int T = blockDim.x;
+    const int part = threadIdx.x % G;
+    for (int e = threadIdx.x / G; e < nodes; e += T / G) {
+        const int inner = e % st;
+        const int alpha = (e / st) % N;
+        const int base = (e / (st * N)) * st * N + inner;
+        double re = 0.0, im = 0.0;
+        for (int x = part; x < N; x += G) {
+            int m = alpha * x;
+            m = pow2 ? (m & (N - 1)) : (m % N);
+            const double c = twc[m], s = sign * tws[m];
+            const double xr = ire[base + x * st], xi = iim[base + x * st];
+            re = fma(xr, c, fma(-xi, s, re));
+            im = fma(xr, s, fma(xi, c, im));
+        }
+        if (G > 1) {
+            const unsigned mask = __activemask();
+            for (int o = G >> 1; o > 0; o >>= 1) {
+                re += __shfl_xor_sync(mask, re, o, G);
+                im += __shfl_xor_sync(mask, im, o, G);
+            }
+        }
+        if (part == 0) {
+            ore[e] = re;
+            oim[e] = im;
+        }
+    }
+    __syncthreads();
+}
+
+// d = 1 tail: the Poisson solve + spline fit is a circulant operator on the
+// nodal density (poisson.py:105-110 + spline.py:78-84 are diagonal in Fourier
+// space), so the coefficient slab is one circular convolution c = gc (*) rho'
+// and the nodal potential phi = gp (*) rho' another; the electric energy follows
+// from Parseval, W = (L/N)/2 sum_i rho'_i phi_i = L/2 sum_alpha k^2 |phi_hat|^2
+// (poisson.py:115-120).  Two length-N convolutions replace two DFT pairs and
+// need far fewer barriers -- this routine sits on the latency-critical path of
+// every d = 1 step.
+static __device__ __forceinline__ bool field_update_1d_body(const FieldParams &p, double *sm) {
+    const int N = p.N, T = blockDim.x, B = p.B, rpb = p.rows_per_block;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double *sb = sm;            // B * N block sums
+    double *r = sb + B * N;     // rho (then neutral rho)
+    double *gc = r + N, *gp = gc + N, *c = gp + N, *phi = c + N;
+    double *scratch = phi + N;  // 64
+    NUFI_STAMP(p, 0);
+    for (int m = threadIdx.x; m < N; m += T) {
+        gc[m] = p.gc[m];
+        gp[m] = p.gp[m];
+    }
+    // ---- block sums over the block's rows in order (reduce_blocks_kernel order) ----
+    double mn = DBL_MAX, mx = -DBL_MAX;
+    if (p.sums) {
+        for (int it = threadIdx.x; it < B * N; it += T) {
+            const int b = it / N, i = it - b * N;
+            const double *src = p.sums + (size_t)b * rpb * N + i;
+            double Sb = 0.0;
+            int q = 0;
+            for (; q + 8 <= rpb; q += 8) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (size_t)(q + u) * N);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) Sb += v[u];
+            }
+            for (; q < rpb; ++q) Sb += __ldcg(src + (size_t)q * N);
+            sb[it] = Sb;
+        }
+        for (int q = threadIdx.x; q < B * p.mm_per_block; q += T) {
+            mn = fmin(mn, __ldcg(p.minmax + 2 * q));
+            mx = fmax(mx, __ldcg(p.minmax + 2 * q + 1));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (lane == 0) {
+            scratch[warp] = mn;
+            scratch[32 + warp] = mx;
+        }
+    } else {
+        for (int i = threadIdx.x; i < N; i += T) r[i] = p.rho_in[i];
+    }
+    __syncthreads();
+    NUFI_STAMP(p, 1);
+    // ---- rho = rho_bar - hv S (density.py:81), mean and min / max in warp 0 ----
+    if (p.sums)
+        for (int i = threadIdx.x; i < N; i += T) {
+            double S = 0.0;
+            for (int b = 0; b < B; ++b) S += sb[b * N + i];
+            r[i] = p.rho_bar - p.hv_d * S;
+        }
+    __syncthreads();
+    if (warp == 0) {
+        double s = 0.0;
+        for (int i = lane; i < N; i += 32) s += r[i];
+        s = warp_sum(s);
+        double fmn = DBL_MAX, fmx = -DBL_MAX;
+        if (p.sums)
+            for (int w = 0; w < (T >> 5); ++w) {
+                fmn = fmin(fmn, scratch[w]);
+                fmx = fmax(fmx, scratch[32 + w]);
+            }
+        if (lane == 0) {
+            const double neut = p.sums ? s / (double)N : 0.0;  // density.py:84
+            scratch[0] = neut;
+            if (p.stats_out) {
+                p.stats_out[0] = neut;
+                p.stats_out[1] = fmn;
+                p.stats_out[2] = fmx;
+            }
+        }
+    }
+    __syncthreads();
+    const double neut = scratch[0];
+    for (int i = threadIdx.x; i < N; i += T) {
+        const double v = r[i] - neut;  // density.py:85
+        r[i] = v;
+        if (p.rho_out) p.rho_out[i] = v;
+    }
+    if (p.finish_only) return true;
+    __syncthreads();
+    NUFI_STAMP(p, 2);
+    // ---- c = gc (*) rho', phi = gp (*) rho': 2N outputs, G lanes each ----
+    {
+        int G = 1;
+        while (G < 32 && 2 * G <= N && 2 * N * (2 * G) <= T) G *= 2;
+        const int part = threadIdx.x % G;
+        for (int o = threadIdx.x / G; o < 2 * N; o += T / G) {
+            const int j = o < N ? o : o - N;
+            const double *g = o < N ? gc : gp;
+            double a0 = 0.0, a1 = 0.0;
+            int i = part;
+            for (; i + G < N; i += 2 * G) {
+                a0 = fma(g[(j - i + N) & (N - 1)], r[i], a0);
+                a1 = fma(g[(j - i - G + N) & (N - 1)], r[i + G], a1);
+            }
+            if (i < N) a0 = fma(g[(j - i + N) & (N - 1)], r[i], a0);
+            double a = a0 + a1;
+            if (G > 1) {
+                const unsigned mask = __activemask();
+                for (int q = G >> 1; q > 0; q >>= 1) a += __shfl_xor_sync(mask, a, q, G);
+            }
+            if (part == 0) (o < N ? c : phi)[j] = a;
+        }
+    }
+    __syncthreads();
+    NUFI_STAMP(p, 4);
+    // ---- W (Parseval) and the neutrality check (poisson.py:97-104) in warp 0 ----
+    if (warp == 0) {
+        double w = 0.0, s = 0.0, m = 0.0;
+        for (int i = lane; i < N; i += 32) {
+            w = fma(r[i], phi[i], w);
+            s += r[i];
+            m = fmax(m, fabs(r[i]));
+        }
+        w = warp_sum(w);
+        s = warp_sum(s);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0) {
+            const bool bad = fabs(s / (double)N) > 1e-8 * m;
+            scratch[1] = bad ? 1.0 : 0.0;
+            if (bad && p.status) *p.status = NUFI_ERR_NUMERICAL;
+            if (!bad && p.W_out) *p.W_out = 0.5 * (p.L / (double)N) * w;
+        }
+    }
+    __syncthreads();
+    NUFI_STAMP(p, 6);
+    if (scratch[1] != 0.0) return false;  // history unchanged (the reference raises before appending)
+    // ---- append: raw slab, evaluation slab (trace_common.cuh layout), E at the nodes ----
+    const double evs = p.slot == 0 ? 0.5 : 1.0;  // slab 0 stored pre-halved
+    double *evg = p.ev_hist ? p.ev_hist + (size_t)p.slot * p.ev_slab_elems : nullptr;
+    double *evl = p.ev_local;
+    double *hrow = p.hist ? p.hist + (size_t)p.slot * N : nullptr;
+    for (int i = threadIdx.x; i < N; i += T) {
+        const double c0 = c[(i - 1 + N) & (N - 1)], c1 = c[i], c2 = c[(i + 1) & (N - 1)], c3 = c[(i + 2) & (N - 1)];
+        const double g0 = 0.5 * (c2 - c0);
+        const double g1 = (c0 - 2.0 * c1) + c2;
+        const double g2 = (1.5 * (c1 - c2)) + 0.5 * (c3 - c0);
+        const double K = evs * p.K;
+        const double A = K * ((g0 + 0.5 * g1) + 0.25 * g2), Bc = K * (g1 + g2), C = K * g2;
+        if (evg) {
+            evg[i] = A;
+            evg[N + i] = Bc;
+            evg[2 * N + i] = C;
+        }
+        if (evl) {
+            evl[i] = A;
+            evl[N + i] = Bc;
+            evl[2 * N + i] = C;
+        }
+        if (hrow) hrow[i] = c1;
+        if (p.coeffs_out) p.coeffs_out[i] = c1;
+        // E(x_i) = -(N/L) (-c_{i-1}/2 + c_{i+1}/2)  (f = 0 stencil, kernels.py:102-123)
+        if (p.E_out) p.E_out[i] = -(0.5 * (c2 - c0)) * p.inv_h;
+    }
+    if (threadIdx.x == 0) {
+        for (int e = 3 * N; e < p.ev_slab_elems; ++e) {
+            if (evg) evg[e] = 0.0;
+            if (evl) evl[e] = 0.0;
+        }
+        if (p.hist_len) *p.hist_len = p.slot + 1;
+    }
+    NUFI_STAMP(p, 8);
+    return true;
+}
+
+// The whole tail.  `sm`: field_smem_doubles(nodes, N, rows_per_block > 1) doubles of shared memory
+// (B <= 8 when rows_per_block > 1).
+static __device__ __forceinline__ bool field_update_body(const FieldParams &p, double *sm) {
+    if (p.d == 1 && p.gc != nullptr && (p.N & (p.N - 1)) == 0 && p.B <= 8) return field_update_1d_body(p, sm);
+    const int nodes = p.nodes, N = p.N, d = p.d, T = blockDim.x;
+    double *re0 = sm, *im0 = re0 + nodes, *re1 = im0 + nodes, *im1 = re1 + nodes;
+    double *twc = im1 + nodes, *tws = twc + N, *sb = tws + N;
+    double *scratch = sb + (p.rows_per_block > 1 ? 8 * nodes : 0);
+    const bool pow2 = (N & (N - 1)) == 0;
+    NUFI_STAMP(p, 0);
+    for (int m = threadIdx.x; m < N; m += T) {
+        twc[m] = p.twc[m];  // tables may live in global or shared memory (generic loads)
+        tws[m] = p.tws[m];
+    }
+
+    // ---- rho: fixed-order combine of the v-sums (density.py:80-81), neutralise (:84-85) ----
+    double neut = 0.0, fmn = 0.0, fmx = 0.0;
+    if (p.sums) {
+        // per-block sums over the block's rows in order (same order as
+        // reduce_blocks_kernel), all (block, node) items in parallel, loads batched
+        const int rpb = p.rows_per_block;
+        if (rpb > 1) {
+            for (int it = threadIdx.x; it < p.B * nodes; it += T) {
+                const int b = it / nodes, i = it % nodes;
+                const double *src = p.sums + (size_t)b * rpb * nodes + i;
+                double Sb = 0.0;
+                int r = 0;
+                for (; r + 8 <= rpb; r += 8) {
+                    double v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (size_t)(r + u) * nodes);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) Sb += v[u];
+                }
+                for (; r < rpb; ++r) Sb += __ldcg(src + (size_t)r * nodes);
+                sb[it] = Sb;
+            }
+            __syncthreads();
+        }
+        NUFI_STAMP(p, 1);
+        double local = 0.0;
+        for (int i = threadIdx.x; i < nodes; i += T) {
+            double S = 0.0;
+            for (int b = 0; b < p.B; ++b) S += rpb > 1 ? sb[b * nodes + i] : __ldcg(p.sums + (size_t)b * nodes + i);
+            const double r = p.rho_bar - p.hv_d * S;
+            re1[i] = r;
+            local += r;
+        }
+        neut = cta_sum(local, scratch) / (double)nodes;
+        double mn = DBL_MAX, mx = -DBL_MAX;
+        const int mrows = p.B * p.mm_per_block;
+        for (int r = threadIdx.x; r < mrows; r += T) {
+            mn = fmin(mn, __ldcg(p.minmax + 2 * r));
+            mx = fmax(mx, __ldcg(p.minmax + 2 * r + 1));
+        }
+        fmx = cta_max(mx, scratch);
+        fmn = -cta_max(-mn, scratch);
+        for (int i = threadIdx.x; i < nodes; i += T) {
+            re0[i] = re1[i] - neut;
+            im0[i] = 0.0;
+        }
+    } else {
+        for (int i = threadIdx.x; i < nodes; i += T) {
+            re0[i] = p.rho_in[i];
+            im0[i] = 0.0;
+        }
+    }
+    __syncthreads();
+    if (p.rho_out)
+        for (int i = threadIdx.x; i < nodes; i += T) p.rho_out[i] = re0[i];
+    if (p.stats_out && threadIdx.x == 0) {
+        p.stats_out[0] = neut;
+        p.stats_out[1] = fmn;
+        p.stats_out[2] = fmx;
+    }
+    if (p.finish_only) return true;
+    NUFI_STAMP(p, 2);
+
+    // ---- neutrality check (poisson.py:97-104) ----
+    {
+        double s = 0.0, mx = 0.0;
+        for (int i = threadIdx.x; i < nodes; i += T) {
+            s += re0[i];
+            mx = fmax(mx, fabs(re0[i]));
+        }
+        const double mean = cta_sum(s, scratch) / (double)nodes;
+        const double tol = 1e-8 * cta_max(mx, scratch);
+        if (fabs(mean) > tol) {
+            if (threadIdx.x == 0 && p.status) *p.status = NUFI_ERR_NUMERICAL;
+            return false;  // history unchanged (the reference raises before appending)
+        }
+    }
+
+    NUFI_STAMP(p, 3);
+    int G = 1;
+    while (G < 32 && 2 * G <= N && (long long)nodes * 2 * G <= T) G *= 2;
+
+    // ---- forward DFT (poisson.py:77) ----
+    double *ar = re0, *ai = im0, *br = re1, *bi = im1;
+    for (int axis = d - 1; axis >= 0; --axis) {
+        int st = 1;
+        for (int a = axis + 1; a < d; ++a) st *= N;
+        dft_pass(ar, ai, br, bi, twc, tws, N, nodes, st, -1.0, G, pow2);
+        double *tr = ar, *ti = ai;
+        ar = br, ai = bi, br = tr, bi = ti;
+    }
+    NUFI_STAMP(p, 4);
+    // ---- phi_hat = rho_hat / k^2, Nyquist / zero mode dropped (poisson.py:105-110);
+    //      W = L^d/2 sum k^2 |phi_hat|^2 (poisson.py:119-120); coefficient spectrum ----
+    double wsum = 0.0;
+    for (int e = threadIdx.x; e < nodes; e += T) {
+        // fac = 1 / (N^d k^2 prod_a sym(alpha_a)) (0 for the zero / Nyquist modes):
+        // (pr, pi) is the coefficient spectrum, (pr, pi) * prod sym is phi_hat
+        const double f = p.fac[e], k2 = p.k2[e], sp = p.fac[nodes + e];
+        const double pr = ar[e] * f, pi = ai[e] * f;
+        ar[e] = pr;
+        ai[e] = pi;
+        const double hr = pr * sp, hi = pi * sp;
+        wsum += k2 * (hr * hr + hi * hi);
+    }
+    const double W = 0.5 * p.L_d * cta_sum(wsum, scratch);
+    if (p.W_out && threadIdx.x == 0) *p.W_out = W;
+
+    NUFI_STAMP(p, 5);
+    // ---- inverse DFT (unscaled) -> spline coefficients (spline.py:84 .real) ----
+    for (int axis = d - 1; axis >= 0; --axis) {
+        int st = 1;
+        for (int a = axis + 1; a < d; ++a) st *= N;
+        dft_pass(ar, ai, br, bi, twc, tws, N, nodes, st, 1.0, G, pow2);
+        double *tr = ar, *ti = ai;
+        ar = br, ai = bi, br = tr, bi = ti;
+    }
+    const double *c = ar;
+    NUFI_STAMP(p, 6);
+
+    // ---- append: raw slab + evaluation slab (spline.py:132-142) ----
+    if (p.hist) {
+        double *hrow = p.hist + (size_t)p.slot * nodes;
+        for (int i = threadIdx.x; i < nodes; i += T) {
+            hrow[i] = c[i];
+            if (p.coeffs_out) p.coeffs_out[i] = c[i];
+        }
+    }
+    double *evg = p.ev_hist ? p.ev_hist + (size_t)p.slot * p.ev_slab_elems : nullptr;
+    double *evl = p.ev_local;
+    auto put = [&](int e, double v) {
+        if (evg) evg[e] = v;
+        if (evl) evl[e] = v;
+    };
+    // slab 0 is only ever used for the final half kick (kernels.py:203-205): store it halved
+    const double evs = p.slot == 0 ? 0.5 : 1.0;
+    if (d == 1) {
+        for (int i = threadIdx.x; i < N; i += T) {
+            const double c0 = c[(i - 1 + N) % N], c1 = c[i], c2 = c[(i + 1) % N], c3 = c[(i + 2) % N];
+            const double g0 = 0.5 * (c2 - c0);
+            const double g1 = (c0 - 2.0 * c1) + c2;
+            const double g2 = (1.5 * (c1 - c2)) + 0.5 * (c3 - c0);
+            const double K = evs * p.K;
+            put(i, K * ((g0 + 0.5 * g1) + 0.25 * g2));
+            put(N + i, K * (g1 + g2));
+            put(2 * N + i, K * g2);
+        }
+    } else {
+        const int row = N + 3, rows = nodes / N;
+        for (int e = threadIdx.x; e < rows * row; e += T) {
+            const int r = e / row, j = e % row;
+            put(e, evs * c[r * N + (j - 1 + N) % N]);
+        }
+    }
+    for (int e = ev_slab_raw_elems(d, N) + threadIdx.x; e < p.ev_slab_elems; e += T) put(e, 0.0);
+    if (threadIdx.x == 0 && p.hist_len) *p.hist_len = p.slot + 1;
+
+    NUFI_STAMP(p, 7);
+    // ---- E at the nodes: -grad of the spline at x_i (f = 0 stencil (1/6, 2/3, 1/6) / (-1/2, 0, 1/2)) ----
+    if (p.E_out) {
+        const double w0[3] = {1.0 / 6.0, 2.0 / 3.0, 1.0 / 6.0};
+        const double dw0[3] = {-0.5, 0.0, 0.5};
+        for (int i = threadIdx.x; i < nodes; i += T) {
+            int idx[3] = {0, 0, 0};
+            int r = i;
+            for (int a = d - 1; a >= 0; --a) {
+                idx[a] = r % N;
+                r /= N;
+            }
+            const int taps = d == 1 ? 3 : (d == 2 ? 9 : 27);
+            for (int g = 0; g < d; ++g) {
+                double acc = 0.0;
+                for (int t = 0; t < taps; ++t) {
+                    const int o[3] = {t % 3, (t / 3) % 3, t / 9};
+                    if (o[g] == 1) continue;  // dw = 0 at the centre tap
+                    int lin = 0;
+                    double w = 1.0;
+                    for (int a = 0; a < d; ++a) {
+                        lin = lin * N + (idx[a] + o[a] - 1 + N) % N;
+                        w *= (a == g) ? dw0[o[a]] : w0[o[a]];
+                    }
+                    acc = fma(c[lin], w, acc);
+                }
+                p.E_out[(size_t)i * d + g] = -acc * p.inv_h;
+            }
+        }
+    }
+    NUFI_STAMP(p, 8);
+    return true;
+}
+
+}  // namespace nufi

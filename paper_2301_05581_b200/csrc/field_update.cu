@@ -1,264 +1,90 @@
-// field_update.cu -- the per-step tail of the NuFI loop on one CTA.
+// field_update.cu -- the per-step tail kernel (one CTA) and its constant tables.
 //
-// Replaces, per step:
-//   density.compute_rho's combine + neutralisation   density.py:80-85
-//   poisson.solve_poisson                             poisson.py:90-112
-//   spline.fit_spline                                 spline.py:71-86
-//   PotentialHistory.append                           spline.py:132-142
-//   poisson.electric_energy                           poisson.py:115-120
-//   E at the nodes (SplineField.eval_E_many)          spline.py:50-52, kernels.py:102-123
-// The spectral steps are separable shared-memory DFTs (Nx^d <= 4096, exact
-// integer twiddle indices).  fit_spline's forward FFT of phi is fused away: for
-// real rho the spectrum of phi is phi_hat * N^d, so the coefficient slab is
-// Re IDFT(phi_hat / prod_a sym(alpha_a)) (same maths as poisson.py:85-87 then
-// spline.py:78-84, one transform pair instead of two).
-//
-// Outputs: coefficient slab -> hist[n], evaluation slab -> ev_hist[n]
-// (layouts in trace_common.cuh), rho, W, E, stats, status.
+// The routine itself is field_update_body (field_common.cuh); this file holds
+// the standalone launch used for d = 2, 3, multi-rank steps and
+// nufi_field_update, the per-handle tables, the evaluation-slab builder for
+// loaded / appended histories, and the device background density.
 #include <cfloat>
 
-#include "trace_common.cuh"
+#include "field_common.cuh"
 
 namespace nufi {
 
-
-
-// block-wide fixed-order sum (deterministic for a fixed blockDim)
-__device__ double block_sum(double v, double *scratch) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    __syncthreads();
-    if (lane == 0) scratch[warp] = v;
-    __syncthreads();
-    double s = 0.0;
-    for (int w = 0; w < nw; ++w) s += scratch[w];
-    __syncthreads();
-    return s;
-}
-
-__device__ double block_max(double v, double *scratch) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
-    __syncthreads();
-    if (lane == 0) scratch[warp] = v;
-    __syncthreads();
-    double s = -DBL_MAX;
-    for (int w = 0; w < nw; ++w) s = fmax(s, scratch[w]);
-    __syncthreads();
-    return s;
-}
-
-// One separable DFT pass along `axis` (stride st): out = sum_x in[x] e^{sign i 2 pi alpha x / N}
-__device__ void dft_pass(const double *__restrict__ ire, const double *__restrict__ iim, double *__restrict__ ore,
-                         double *__restrict__ oim, const double *__restrict__ twc, const double *__restrict__ tws,
-                         int N, int nodes, int st, double sign, bool pow2) {
-    for (int e = threadIdx.x; e < nodes; e += blockDim.x) {
-        const int inner = e % st;
-        const int alpha = (e / st) % N;
-        const int base = (e / (st * N)) * st * N + inner;
-        double re = 0.0, im = 0.0;
-        for (int x = 0; x < N; ++x) {
-            int m = alpha * x;
-            m = pow2 ? (m & (N - 1)) : (m % N);
-            const double c = twc[m], s = sign * tws[m];
-            const double xr = ire[base + x * st], xi = iim[base + x * st];
-            re = fma(xr, c, fma(-xi, s, re));
-            im = fma(xr, s, fma(xi, c, im));
-        }
-        ore[e] = re;
-        oim[e] = im;
-    }
-    __syncthreads();
-}
-
-__device__ __forceinline__ int fftfreq(int alpha, int N) { return alpha < (N + 1) / 2 ? alpha : alpha - N; }
-
-// dynamic smem: re0, im0, re1, im1 (nodes each), twc, tws (N each), scratch (32)
 __global__ void __launch_bounds__(1024) field_update_kernel(const FieldParams p) {
     extern __shared__ __align__(16) double fsm[];
-    const int nodes = p.nodes, N = p.N, d = p.d;
-    double *re0 = fsm, *im0 = re0 + nodes, *re1 = im0 + nodes, *im1 = re1 + nodes;
-    double *twc = im1 + nodes, *tws = twc + N, *scratch = tws + N;
-    const bool pow2 = (N & (N - 1)) == 0;
+    field_update_body(p, fsm);
+}
 
-    for (int m = threadIdx.x; m < N; m += blockDim.x) {
+// d = 1 (field_update_1d_body) stages up to 8 block-sum rows; d = 2, 3 read the block table directly
+size_t field_update_smem_bytes(int d, int nodes, int N) {
+    return (size_t)field_smem_doubles(nodes, N, d == 1) * sizeof(double);
+}
+
+cudaError_t launch_field_update(const FieldParams &p, cudaStream_t st) {
+    const size_t smem = field_update_smem_bytes(p.d, p.nodes, p.N);
+    cudaError_t e = cudaFuncSetAttribute(field_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int threads = p.nodes >= 1024 ? 1024 : (p.nodes >= 128 ? 512 : 256);
+    field_update_kernel<<<1, threads, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+// Constant tables of field_common.cuh: tw[0:N] = cos(2 pi m/N), tw[N:2N] = sin;
+// fac[e] = 1 / (N^d k^2 prod_a sym(alpha_a)) with k^2 = sum_a (2 pi m_a / L)^2
+// (poisson.py:52-59, m = fftfreq) and sym(alpha) = (4 + 2 cos(2 pi alpha / N)) / 6
+// (spline.py:20-25); 0 at the zero mode and wherever an axis carries the
+// Nyquist mode (poisson.py:62-69, 106-110); fac[nodes + e] = prod_a sym.
+__global__ void field_tables_kernel(double *tw, double *fac, double *k2t, int d, int N, int nodes, double k_scale) {
+    for (int m = threadIdx.x + blockIdx.x * blockDim.x; m < N; m += blockDim.x * gridDim.x) {
         double s, c;
         sincospi(2.0 * (double)m / (double)N, &s, &c);
-        twc[m] = c;
-        tws[m] = s;
+        tw[m] = c;
+        tw[N + m] = s;
     }
-
-    // ---- rho: fixed-order combine of the v-block sums, then neutralise ----
-    double neut = 0.0, fmn = 0.0, fmx = 0.0;
-    if (p.partials) {
-        double local = 0.0;
-        for (int i = threadIdx.x; i < nodes; i += blockDim.x) {
-            double S = 0.0;
-            for (int b = 0; b < p.B; ++b) S += p.partials[(size_t)b * nodes + i];
-            const double r = p.rho_bar - p.hv_d * S;  // density.py:81
-            re1[i] = r;
-            local += r;
-        }
-        neut = block_sum(local, scratch) / (double)nodes;  // density.py:84 rho.mean()
-        fmn = DBL_MAX;
-        fmx = -DBL_MAX;
-        const double *mm = p.partials + (size_t)p.B * nodes;
-        for (int b = 0; b < p.B; ++b) {
-            fmn = fmin(fmn, mm[2 * b]);
-            fmx = fmax(fmx, mm[2 * b + 1]);
-        }
-        for (int i = threadIdx.x; i < nodes; i += blockDim.x) {
-            re0[i] = re1[i] - neut;  // density.py:85
-            im0[i] = 0.0;
-        }
-    } else {
-        for (int i = threadIdx.x; i < nodes; i += blockDim.x) {
-            re0[i] = p.rho_in[i];
-            im0[i] = 0.0;
-        }
-    }
-    __syncthreads();
-
-    if (p.rho_out)
-        for (int i = threadIdx.x; i < nodes; i += blockDim.x) p.rho_out[i] = re0[i];
-    if (p.stats_out && threadIdx.x == 0) {
-        p.stats_out[0] = neut;
-        p.stats_out[1] = fmn;
-        p.stats_out[2] = fmx;
-    }
-    if (p.finish_only) return;
-    // ---- neutrality check (poisson.py:97-104) ----
-    {
-        double s = 0.0, mx = 0.0;
-        for (int i = threadIdx.x; i < nodes; i += blockDim.x) {
-            s += re0[i];
-            mx = fmax(mx, fabs(re0[i]));
-        }
-        const double mean = block_sum(s, scratch) / (double)nodes;
-        const double tol = 1e-8 * block_max(mx, scratch);
-        if (fabs(mean) > tol) {
-            if (threadIdx.x == 0) *p.status = NUFI_ERR_NUMERICAL;
-            return;  // history unchanged (the reference raises before appending)
-        }
-    }
-
-    // ---- forward DFT of rho over every axis (poisson.py:77) ----
-    double *ar = re0, *ai = im0, *br = re1, *bi = im1;
-    for (int axis = d - 1; axis >= 0; --axis) {
-        int st = 1;
-        for (int a = axis + 1; a < d; ++a) st *= N;
-        dft_pass(ar, ai, br, bi, twc, tws, N, nodes, st, -1.0, pow2);
-        double *tr = ar, *ti = ai;
-        ar = br;
-        ai = bi;
-        br = tr;
-        bi = ti;
-    }
-    // spectrum in (ar, ai); phi_hat = rho_hat / k^2 (poisson.py:105-110), energy, coefficient spectrum
-    double wsum = 0.0;
-    const double inv_nodes = 1.0 / (double)nodes;
-    for (int e = threadIdx.x; e < nodes; e += blockDim.x) {
+    for (int e = threadIdx.x + blockIdx.x * blockDim.x; e < nodes; e += blockDim.x * gridDim.x) {
         double k2 = 0.0, symp = 1.0;
         bool nyq = false;
         int r = e;
         for (int a = d - 1; a >= 0; --a) {
             const int alpha = r % N;
             r /= N;
-            const int m = fftfreq(alpha, N);
-            const double km = p.k_scale * (double)m;
+            const int m = alpha < (N + 1) / 2 ? alpha : alpha - N;
+            const double km = k_scale * (double)m;
             k2 += km * km;
-            if ((N % 2 == 0) && (m == N / 2 || m == -N / 2)) nyq = true;
-            symp *= (4.0 + 2.0 * cospi(2.0 * (double)alpha / (double)N)) / 6.0;  // spline.py:20-25
+            if ((N % 2 == 0) && (m == -N / 2)) nyq = true;
+            symp *= (4.0 + 2.0 * cospi(2.0 * (double)alpha / (double)N)) / 6.0;
         }
-        double pr = 0.0, pi = 0.0;
-        if (k2 > 0.0 && !nyq) {
-            pr = ar[e] * inv_nodes / k2;
-            pi = ai[e] * inv_nodes / k2;
-        }
-        wsum += k2 * (pr * pr + pi * pi);  // poisson.py:119
-        ar[e] = pr / symp;
-        ai[e] = pi / symp;
+        k2t[e] = k2;
+        fac[e] = (k2 > 0.0 && !nyq) ? 1.0 / ((double)nodes * k2 * symp) : 0.0;
+        fac[nodes + e] = symp;
     }
-    const double W = 0.5 * p.L_d * block_sum(wsum, scratch);  // poisson.py:120
-    if (p.W_out && threadIdx.x == 0) *p.W_out = W;
+}
 
-    // ---- inverse DFT (unscaled) -> spline coefficients (real part) ----
-    for (int axis = d - 1; axis >= 0; --axis) {
-        int st = 1;
-        for (int a = axis + 1; a < d; ++a) st *= N;
-        dft_pass(ar, ai, br, bi, twc, tws, N, nodes, st, 1.0, pow2);
-        double *tr = ar, *ti = ai;
-        ar = br;
-        ai = bi;
-        br = tr;
-        bi = ti;
+// d = 1 circulant kernels: gc[m] = sum_alpha fac[alpha] cos(2 pi alpha m / N)
+// (coefficients, spline.py:78-84 o poisson.py:105-110) and
+// gp[m] = sum_alpha fac[alpha] sym[alpha] cos(2 pi alpha m / N) (nodal potential,
+// poisson.py:85-87); fac already carries the 1/N of the inverse transform.
+__global__ void field_conv_kernels_kernel(const double *fac, double *gc, double *gp, int N) {
+    for (int m = threadIdx.x + blockIdx.x * blockDim.x; m < N; m += blockDim.x * gridDim.x) {
+        double a = 0.0, b = 0.0;
+        for (int al = 0; al < N; ++al) {
+            const double cs = cospi(2.0 * (double)((al * m) % N) / (double)N);
+            a = fma(fac[al], cs, a);
+            b = fma(fac[al] * fac[N + al], cs, b);
+        }
+        gc[m] = a;
+        gp[m] = b;
     }
-    const double *c = ar;  // coefficient slab (Nx,)*d row-major
+}
 
-    // ---- append: raw slab, evaluation slab (spline.py:132-142) ----
-    double *hrow = p.hist + (size_t)p.slot * nodes;
-    for (int i = threadIdx.x; i < nodes; i += blockDim.x) {
-        hrow[i] = c[i];
-        if (p.coeffs_out) p.coeffs_out[i] = c[i];
-    }
-    double *ev = p.ev_hist + (size_t)p.slot * p.ev_slab_elems;
-    if (d == 1) {
-        // cell i, centred fc: kick = K * g(fc + 1/2), g = sum_taps c * dw  (kernels.py:164-182)
-        for (int i = threadIdx.x; i < N; i += blockDim.x) {
-            const double c0 = c[(i - 1 + N) % N], c1 = c[i], c2 = c[(i + 1) % N], c3 = c[(i + 2) % N];
-            const double g0 = 0.5 * (c2 - c0);
-            const double g1 = (c0 - 2.0 * c1) + c2;
-            const double g2 = (1.5 * (c1 - c2)) + 0.5 * (c3 - c0);
-            ev[i] = p.K * ((g0 + 0.5 * g1) + 0.25 * g2);
-            ev[N + i] = p.K * (g1 + g2);
-            ev[2 * N + i] = p.K * g2;
-        }
-    } else {
-        const int row = N + 3;
-        const int rows = nodes / N;
-        for (int e = threadIdx.x; e < rows * row; e += blockDim.x) {
-            const int r = e / row, j = e % row;
-            ev[e] = c[r * N + (j - 1 + N) % N];
-        }
-    }
-    if (threadIdx.x == 0) {
-        const int raw = ev_slab_raw_elems(d, N);
-        for (int e = raw; e < p.ev_slab_elems; ++e) ev[e] = 0.0;
-        if (p.hist_len) *p.hist_len = p.slot + 1;
-    }
-
-    // ---- E at the nodes: -grad of the spline at x_i (f = 0 stencil) ----
-    if (p.E_out) {
-        const double w0[3] = {1.0 / 6.0, 2.0 / 3.0, 1.0 / 6.0};
-        const double dw0[3] = {-0.5, 0.0, 0.5};
-        for (int i = threadIdx.x; i < nodes; i += blockDim.x) {
-            int idx[3] = {0, 0, 0};
-            {
-                int r = i;
-                for (int a = d - 1; a >= 0; --a) {
-                    idx[a] = r % N;
-                    r /= N;
-                }
-            }
-            for (int g = 0; g < d; ++g) {
-                double acc = 0.0;
-                const int taps = d == 1 ? 3 : (d == 2 ? 9 : 27);
-                for (int t = 0; t < taps; ++t) {
-                    int o[3] = {t % 3, (t / 3) % 3, t / 9};
-                    int lin = 0;
-                    double w = 1.0;
-                    for (int a = 0; a < d; ++a) {
-                        lin = lin * N + (idx[a] + o[a] - 1 + N) % N;
-                        w *= (a == g) ? dw0[o[a]] : w0[o[a]];
-                    }
-                    acc = fma(c[lin], w, acc);
-                }
-                p.E_out[(size_t)i * d + g] = -acc * p.inv_h;
-            }
-        }
-    }
+cudaError_t launch_field_tables(double *tw, double *fac, double *k2, int d, int N, int nodes, double k_scale,
+                                cudaStream_t st) {
+    field_tables_kernel<<<8, 256, 0, st>>>(tw, fac, k2, d, N, nodes, k_scale);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || d != 1) return e;
+    // d = 1: gc, gp follow k2 in the table buffer
+    field_conv_kernels_kernel<<<1, 256, 0, st>>>(fac, k2 + nodes, k2 + nodes + N, N);
+    return cudaGetLastError();
 }
 
 // Evaluation slabs (trace_common.cuh layouts) for raw rows [r0, r1) of hist.
@@ -267,7 +93,9 @@ __global__ void build_ev_slabs_kernel(const double *__restrict__ hist, double *_
     const int64_t slot = r0 + blockIdx.x;
     const double *c = hist + (size_t)slot * nodes;
     double *ev = ev_hist + (size_t)slot * ev_slab_elems;
+    const double evs = slot == 0 ? 0.5 : 1.0;  // slab 0 stored pre-halved (field_common.cuh)
     if (d == 1) {
+        K *= evs;
         for (int i = threadIdx.x; i < N; i += blockDim.x) {
             const double c0 = c[(i - 1 + N) % N], c1 = c[i], c2 = c[(i + 1) % N], c3 = c[(i + 2) % N];
             const double g0 = 0.5 * (c2 - c0);
@@ -282,7 +110,7 @@ __global__ void build_ev_slabs_kernel(const double *__restrict__ hist, double *_
         const int rows = nodes / N;
         for (int e = threadIdx.x; e < rows * row; e += blockDim.x) {
             const int r = e / row, j = e % row;
-            ev[e] = c[r * N + (j - 1 + N) % N];
+            ev[e] = evs * c[r * N + (j - 1 + N) % N];
         }
     }
     for (int e = ev_slab_raw_elems(d, N) + threadIdx.x; e < ev_slab_elems; e += blockDim.x) ev[e] = 0.0;
@@ -292,17 +120,6 @@ cudaError_t launch_build_ev_slabs(const double *hist, double *ev_hist, int d, in
                                   double K, int64_t r0, int64_t r1, cudaStream_t st) {
     if (r1 <= r0) return cudaSuccess;
     build_ev_slabs_kernel<<<(unsigned)(r1 - r0), 256, 0, st>>>(hist, ev_hist, d, N, nodes, ev_slab_elems, K, r0);
-    return cudaGetLastError();
-}
-
-size_t field_update_smem_bytes(int nodes, int N) { return (4 * (size_t)nodes + 2 * N + 32) * sizeof(double); }
-
-cudaError_t launch_field_update(const FieldParams &p, cudaStream_t st) {
-    const size_t smem = field_update_smem_bytes(p.nodes, p.N);
-    cudaError_t e = cudaFuncSetAttribute(field_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int threads = p.nodes >= 1024 ? 1024 : (p.nodes >= 256 ? 256 : 128);
-    field_update_kernel<<<1, threads, smem, st>>>(p);
     return cudaGetLastError();
 }
 
@@ -337,7 +154,7 @@ __global__ void __launch_bounds__(1024) rho_bar_kernel(const RhoBarParams p) {
         }
         sv += vel;
     }
-    const double sum_v = block_sum(sv, scratch);
+    const double sum_v = cta_sum(sv, scratch);
     double sx = 0.0;
     for (int64_t i = threadIdx.x; i < X; i += blockDim.x) {
         int64_t r = i;
@@ -349,7 +166,7 @@ __global__ void __launch_bounds__(1024) rho_bar_kernel(const RhoBarParams p) {
         }
         sx += 1.0 + p.f0.alpha * pert;
     }
-    const double sum_x = block_sum(sx, scratch);
+    const double sum_x = cta_sum(sx, scratch);
     if (threadIdx.x == 0) *p.out = sum_x * sum_v * p.hx_d * p.hv_d / p.L_d;
 }
 

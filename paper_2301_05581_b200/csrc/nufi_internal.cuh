@@ -139,6 +139,24 @@ __device__ __forceinline__ void tma_bulk_g2s(void *dst_smem, const void *src_gme
         : "memory");
 }
 
+// Grid-wide barrier for a cooperative (co-resident) launch: monotonically
+// increasing arrival counter, `target` = CTAs x barrier-generation.
+__device__ __forceinline__ void grid_barrier(unsigned *counter, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(counter, 1u);
+        unsigned v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+        while (v < target) {
+            __nanosleep(64);  // back off: do not hammer the counter's L2 slice while others trace
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 // ----------------------------------------------------------------------------
 // kernel parameter blocks
 // ----------------------------------------------------------------------------
@@ -168,30 +186,6 @@ struct TraceRhoParams {
     // outputs: partial[vt][nodes], fminmax[vt * node_tiles + tile][2]
     double *partial;
     double *fminmax;
-};
-
-// per-step tail (field_update.cu)
-struct FieldParams {
-    int d, N, nodes, B;
-    double L, inv_h, hv_d, rho_bar, L_d, K;
-    double k_scale;  // 2*pi/L (poisson.py:54)
-    // inputs (one of the two)
-    const double *partials;  // [B][nodes] sums, then [B][2] (min, max)
-    const double *rho_in;    // neutral rho (nufi_field_update)
-    // step slot
-    int64_t slot;            // history row written
-    double *hist;            // (cap, nodes)
-    double *ev_hist;         // (cap, ev_slab_elems)
-    int ev_slab_elems;
-    // outputs (nullable)
-    double *rho_out;         // nodes
-    double *stats_out;       // 3: neutralization, f_min, f_max
-    double *W_out;           // 1
-    double *E_out;           // nodes * d
-    double *coeffs_out;      // nodes
-    int *status;             // set to NUFI_ERR_NUMERICAL when rho is not neutral
-    int64_t *hist_len;       // device-side history length, set to slot + 1
-    int finish_only;         // compute_rho only: stop after rho / stats
 };
 
 // background density (field_update.cu)

@@ -1,0 +1,292 @@
+// run_1d.cu -- d = 1 whole-run persistent kernel: every step of the NuFI loop
+// in ONE cooperative launch.
+//
+// d = 1 runs are latency-bound: 16-33k points, each step a serial chain of n
+// substeps per point, then a global v-sum, then the Poisson / spline tail whose
+// result the very first substep of the next step needs.  Launch gaps and a
+// serial single-CTA tail would dominate, so:
+//
+//   for n = n_first .. n_last:
+//     trace   every CTA traces its tiles of points through slabs n-1 .. 0:
+//             slab n-1 from its own shared-memory copy, slabs n-2 .. 0 streamed
+//             by the TMA ring (producer warp, cp.async.bulk + mbarriers);
+//             f0 at the foot point; fixed-order CTA v-sum -> partial[vt][node]
+//     barrier grid-wide (co-resident CTAs, monotonic arrival counter)
+//     tail    EVERY CTA runs the same fixed-order combine + Poisson / spline /
+//             W / E (field_common.cuh) on the partials -- redundant but parallel,
+//             so no second barrier: each CTA keeps evaluation slab n in shared
+//             memory for its next step; CTA 0 alone writes the history and the
+//             per-step outputs.
+//
+// Deterministic: every CTA executes the identical tail on identical data.
+#include <cfloat>
+
+#include "field_common.cuh"
+
+namespace nufi {
+
+struct Run1DParams {
+    TraceRhoParams tp;  // geometry / arithmetic (tp.n unused)
+    FieldParams fp;     // tail template (slot and outputs set per step)
+    int n_first, n_last;
+    double *rho_hist, *E_hist, *W_hist, *stats_hist;  // device rows (n - n_first), nullable
+    unsigned *barrier;                                // zero at launch
+    int tiles;                                        // node_tiles * v-tiles
+    unsigned long long *stamps;                       // optional: CTA 0 globaltimer per step x 3
+};
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// One substep with the drift folded into the kick: on entry X is the already
+// drifted position of this substep; on exit X is the drifted position of the
+// next one, X - V_new = (X - V) - A - fc * (B + fc C), so the next cell lookup
+// does not wait for a separate drift DADD.  (Same arithmetic as trace_common.cuh
+// up to rounding order.)
+template <int NX>
+__device__ __forceinline__ void kick1(double &X, double &V, const double *__restrict__ slab, int N) {
+    const double s = X + MAGIC;
+    const int n_ = NX ? NX : N;
+    const char *b = reinterpret_cast<const char *>(slab);
+    const double *c = reinterpret_cast<const double *>(
+        b + (((unsigned)__double_as_longlong(s) & (unsigned)(n_ - 1)) << 3));
+    const double fc = X - (s - MAGIC);
+    const double XmV = X - V;
+    const double A = c[0], B = c[n_], C = c[2 * n_];
+    const double t = fma(fc, C, B);
+    X = fma(-fc, t, XmV - A);
+    V = fma(fc, t, V + A);
+}
+
+__device__ __forceinline__ void kick1_any(double &X, double &V, const double *__restrict__ slab, int N) {
+    double fc;
+    const int i = locate_centred<false>(X, N, fc);
+    const double A = slab[i], t = fma(fc, slab[2 * N + i], slab[N + i]);
+    const double XmV = X - V;
+    X = fma(-fc, t, XmV - A);
+    V = fma(fc, t, V + A);
+}
+
+template <int NX, int SPS>
+__global__ void __launch_bounds__(288, 2) run_1d_kernel(const Run1DParams P) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const TraceRhoParams &p = P.tp;
+    const int cw = (blockDim.x >> 5) - 1;  // consumer warps; the last warp is the TMA producer
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool producer = warp == cw;
+    const int N = NX ? NX : p.N;
+    const int SLAB = NX ? ev_slab_elems(1, NX) : p.ev_slab_elems;
+    const int stages = p.stages;
+    const int nodes = p.nodes;
+
+    // shared memory: ring | barriers | red | local slab | tail workspace
+    double *ring = reinterpret_cast<double *>(smem_raw);
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)stages * SPS * SLAB);
+    uint64_t *empty = full + stages;
+    double *red = reinterpret_cast<double *>(empty + stages);  // 3 * 32 * cw
+    double *slabN = red + 3 * 32 * cw;                          // evaluation slab n-1 (SLAB)
+    double *tail = slabN + SLAB;                                // field_smem_doubles(nodes, N, true)
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], cw);
+        }
+        fence_mbar_init();
+    }
+    if (P.n_first >= 1)
+        for (int e = threadIdx.x; e < SLAB; e += blockDim.x)
+            slabN[e] = __ldcg(p.ev_hist + (size_t)(P.n_first - 1) * SLAB + e);
+    __syncthreads();
+
+    // ring state (identical sequence on the producer and the consumers)
+    int s_ring = 0;
+    uint32_t ph_ring = 0;
+    int fills = 0;
+    unsigned gen = 0;
+
+    for (int n = P.n_first; n <= P.n_last; ++n) {
+        const int m = n >= 1 ? n - 1 : 0;  // slabs streamed by TMA: m-1 .. 0
+        const int groups = (m + SPS - 1) / SPS;
+        const int top_cnt = m - (groups - 1) * SPS;
+
+        for (int tile = blockIdx.x; tile < P.tiles; tile += gridDim.x) {
+            static constexpr bool kAlt = false;  // tile mapping: v-tile-major (true) or node-tile-major
+            const int vts = P.tiles / p.node_tiles;
+            const int nt = kAlt ? tile / vts : tile % p.node_tiles;
+            const int vt = kAlt ? tile % vts : tile / p.node_tiles;
+            const int node = nt * 32 + lane;
+            double acc = 0.0, fmn = DBL_MAX, fmx = -DBL_MAX;
+            if (producer) {
+                if (lane == 0) {
+                    for (int it = 0; it < groups; ++it) {
+                        if (fills >= stages) mbar_wait(&empty[s_ring], ph_ring ^ 1u);
+                        const int k_lo = (groups - 1 - it) * SPS, k_hi = min(m - 1, k_lo + SPS - 1);
+                        const uint32_t bytes = (uint32_t)((k_hi - k_lo + 1) * SLAB * sizeof(double));
+                        mbar_arrive_expect_tx(&full[s_ring], bytes);
+                        tma_bulk_g2s(ring + (size_t)s_ring * SPS * SLAB, p.ev_hist + (size_t)k_lo * SLAB, bytes,
+                                     &full[s_ring]);
+                        ++fills;
+                        if (++s_ring == stages) s_ring = 0, ph_ring ^= 1u;
+                    }
+                } else {
+                    // keep the warp's copy of the ring state in step with lane 0
+                    for (int it = 0; it < groups; ++it) {
+                        ++fills;
+                        if (++s_ring == stages) s_ring = 0, ph_ring ^= 1u;
+                    }
+                }
+            } else {
+                const bool valid = node < nodes;
+                const int j = vt * p.vt_rows + warp;
+                const double v0 = __dadd_rn(-p.vmax, __dmul_rn((double)j + 0.5, p.hv));  // grids.py:110-115
+                double V = v0 * p.vel_to_scaled;
+                double X = ((double)(valid ? node : 0) - 0.5) - V;  // first drift (folded form)
+                if (n >= 1) {
+                    if (NX)
+                        kick1<NX>(X, V, slabN, N);
+                    else
+                        kick1_any(X, V, slabN, N);
+                }
+                long long wait_cyc = 0, t_start = clock64();
+                for (int it = 0; it < groups; ++it) {
+                    const long long tw0 = clock64();
+                    mbar_wait(&full[s_ring], ph_ring);
+                    wait_cyc += clock64() - tw0;
+                    const double *buf = ring + (size_t)s_ring * SPS * SLAB;
+                    if (NX != 0 && (it > 0 || top_cnt == SPS)) {
+#pragma unroll
+                        for (int q = SPS - 1; q >= 0; --q) kick1<NX>(X, V, buf + q * SLAB, N);
+                    } else {
+                        const int cnt = it == 0 ? top_cnt : SPS;
+                        for (int q = cnt - 1; q >= 0; --q) {
+                            if (NX)
+                                kick1<NX>(X, V, buf + q * SLAB, N);
+                            else
+                                kick1_any(X, V, buf + q * SLAB, N);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[s_ring]);
+                    ++fills;
+                    if (++s_ring == stages) s_ring = 0, ph_ring ^= 1u;
+                }
+                if (P.stamps && n == P.n_last && lane == 0 && warp == 0) {
+                    const size_t o = 3 * (size_t)(P.n_last - P.n_first + 1) + 10 + 4 * 1024 + 2 * blockIdx.x;
+                    P.stamps[o] = (unsigned long long)wait_cyc;
+                    P.stamps[o + 1] = (unsigned long long)(clock64() - t_start);
+                }
+                double x, v;
+                if (n == 0) {
+                    x = __dmul_rn((double)node, p.hx);  // grids.py:104-108
+                    v = v0;
+                } else {
+                    x = ((X + V) + 0.5) * p.hx;  // undo the look-ahead drift of the last kick
+                    v = V * p.scaled_to_vel;
+                }
+                const double f = eval_f0<1>(p.f0, &x, &v);
+                if (valid) acc = fmn = fmx = f;
+                red[threadIdx.x] = acc;
+                red[32 * cw + threadIdx.x] = fmn;
+                red[64 * cw + threadIdx.x] = fmx;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                double sum = 0.0, mn = DBL_MAX, mx = -DBL_MAX;
+                for (int w = 0; w < cw; ++w) {
+                    sum += red[w * 32 + lane];
+                    mn = fmin(mn, red[32 * cw + w * 32 + lane]);
+                    mx = fmax(mx, red[64 * cw + w * 32 + lane]);
+                }
+                if (node < nodes) p.partial[(size_t)vt * nodes + node] = sum;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                }
+                if (lane == 0) {
+                    const size_t c = (size_t)vt * p.node_tiles + nt;
+                    p.fminmax[2 * c] = mn;
+                    p.fminmax[2 * c + 1] = mx;
+                }
+            }
+            __syncthreads();
+        }
+
+        // all partials of step n are written
+        if (P.stamps && blockIdx.x == 0 && threadIdx.x == 0) P.stamps[3 * (n - P.n_first)] = globaltimer();
+        if (P.stamps && threadIdx.x == 0 && (n % 400) == 0 && n > 0 && n / 400 <= 4 && blockIdx.x < 1024) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            P.stamps[3 * (P.n_last - P.n_first + 1) + 10 + (n / 400 - 1) * 1024 + blockIdx.x] =
+                (globaltimer() << 8) | (smid & 0xff);
+        }
+        grid_barrier(P.barrier, ++gen * gridDim.x);
+        if (P.stamps && blockIdx.x == 0 && threadIdx.x == 0) P.stamps[3 * (n - P.n_first) + 1] = globaltimer();
+
+        // redundant tail in every CTA; CTA 0 publishes
+        FieldParams fp = P.fp;
+        fp.slot = n;
+        fp.ev_local = slabN;
+        const int64_t row = n - P.n_first;
+        if (blockIdx.x == 0) {
+            fp.rho_out = P.rho_hist ? P.rho_hist + row * nodes : nullptr;
+            fp.E_out = P.E_hist ? P.E_hist + row * nodes : nullptr;
+            fp.W_out = P.W_hist ? P.W_hist + row : nullptr;
+            fp.stats_out = P.stats_hist ? P.stats_hist + row * 3 : nullptr;
+        } else {
+            fp.rho_out = fp.E_out = fp.W_out = fp.stats_out = fp.coeffs_out = nullptr;
+            fp.hist = fp.ev_hist = nullptr;
+            fp.hist_len = nullptr;
+            fp.status = nullptr;
+        }
+        fp.tstamps = (P.stamps && blockIdx.x == 0 && n == P.n_last) ? P.stamps + 3 * (P.n_last - P.n_first + 1) : nullptr;
+        const bool ok = field_update_body(fp, tail);
+        __syncthreads();
+        if (P.stamps && blockIdx.x == 0 && threadIdx.x == 0) P.stamps[3 * (n - P.n_first) + 2] = globaltimer();
+        if (!ok) break;  // identical decision in every CTA
+    }
+}
+
+size_t run_1d_smem_bytes(const TraceRhoParams &p, int threads) {
+    const int cw = threads / 32 - 1;
+    return (size_t)p.stages * p.slabs_per_stage * p.ev_slab_elems * sizeof(double) + 2 * p.stages * sizeof(uint64_t) +
+           (3 * 32 * (size_t)cw + p.ev_slab_elems + field_smem_doubles(p.nodes, p.N, true)) * sizeof(double);
+}
+
+template <int NX, int SPS>
+static cudaError_t launch_run(const Run1DParams &P, int threads, int device, cudaStream_t st, int *grid_out) {
+    auto kern = run_1d_kernel<NX, SPS>;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    size_t smem = run_1d_smem_bytes(P.tp, threads);
+    // latency-bound (tiles <= SMs): one CTA per SM -- reserve more than half the
+    // SM's shared memory so the scheduler cannot double up CTAs on one SM
+    if (P.tiles <= sms && smem < 120 * 1024) smem = 120 * 1024;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const int grid = std::min(P.tiles, per_sm * sms);
+    if (grid_out) *grid_out = grid;
+    Run1DParams args = P;
+    void *kargs[] = {&args};
+    return cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(threads), kargs, smem, st);
+}
+
+cudaError_t launch_run_1d(const Run1DParams &P, int threads, int device, cudaStream_t st, int *grid_out) {
+    switch (P.tp.N) {
+        case 32: return launch_run<32, 16>(P, threads, device, st, grid_out);
+        case 64: return launch_run<64, 16>(P, threads, device, st, grid_out);
+        case 128: return launch_run<128, 8>(P, threads, device, st, grid_out);
+        case 256: return launch_run<256, 4>(P, threads, device, st, grid_out);
+        default: return launch_run<0, 1>(P, threads, device, st, grid_out);
+    }
+}
+
+}  // namespace nufi

@@ -185,8 +185,8 @@ __global__ void trace_points_fast(const double *__restrict__ ev_hist, int ev_sla
     }
     if (half_kick && n > 0) kick<D, POW2>(Xs, Vs, ev_hist + (size_t)n * ev_slab_elems, N, K, true);
     if (n == 0) return;
-    for (int k = n - 1; k >= 1; --k) substep<D, POW2>(Xs, Vs, ev_hist + (size_t)k * ev_slab_elems, N, K, false);
-    substep<D, POW2>(Xs, Vs, ev_hist, N, K, true);
+    // slab 0 is stored pre-halved: the final tau/2 kick needs no special case
+    for (int k = n - 1; k >= 0; --k) substep<D, POW2>(Xs, Vs, ev_hist + (size_t)k * ev_slab_elems, N, K, false);
 #pragma unroll
     for (int a = 0; a < D; ++a) {
         X[p * D + a] = (Xs[a] + 0.5) * hx;

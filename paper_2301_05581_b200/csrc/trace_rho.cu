@@ -109,14 +109,11 @@ __global__ void __launch_bounds__(512) trace_rho_kernel(const TraceRhoParams p, 
             const int k_lo = max(0, k_hi - sps + 1);
             mbar_wait(&full[s], u & 1u);
             const double *buf = ring + (size_t)s * sps * slab_elems;
-            for (int k = k_hi; k >= max(k_lo, 1); --k) {
+            // slab 0 is stored pre-halved (field_common.cuh), so every kick is uniform
+            for (int k = k_hi; k >= k_lo; --k) {
                 const double *slab = buf + (size_t)(k - k_lo) * slab_elems;
 #pragma unroll
                 for (int pp = 0; pp < PPT; ++pp) substep<D, POW2>(X[pp], V[pp], slab, N, K, false);
-            }
-            if (k_lo == 0) {
-#pragma unroll
-                for (int pp = 0; pp < PPT; ++pp) substep<D, POW2>(X[pp], V[pp], buf, N, K, true);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
@@ -257,7 +254,6 @@ cudaError_t launch_trace_rho(int d, int ppt, bool pow2, const TraceRhoParams &p,
     if (d == DD && ppt == PP)                                                                        \
         return pow2 ? launch_one<DD, PP, true>(p, K, ctas, threads, smem, st)                        \
                     : launch_one<DD, PP, false>(p, K, ctas, threads, smem, st);
-    NUFI_TR(1, 1)
     NUFI_TR(2, 1)
     NUFI_TR(3, 1)
     NUFI_TR(2, 2)
