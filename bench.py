@@ -257,7 +257,8 @@ def gpu_arm(args, rank: int, world: int):
     prof = np.zeros(8)
     lib.nufi_profiling_read(h.h, prof.ctypes.data)
     lib.nufi_profiling(h.h, 0)
-    trace_ms, trace_launches, reduce_ms, _, field_ms, _, trace_ps, _ = prof
+    trace_ms, trace_launches, reduce_ms, reduce_launches, field_ms, field_launches, trace_ps, _ = prof
+    launches_per_run = int(trace_launches + reduce_launches + field_launches)
     peak = ctypes.c_double()
     peak_ms = ctypes.c_double()
     lib.nufi_fp64_peak(dev, ctypes.byref(peak), ctypes.byref(peak_ms))
@@ -265,7 +266,8 @@ def gpu_arm(args, rank: int, world: int):
     roofline = {
         "bound": "fp64", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
         "frac": achieved / peak.value if peak.value else None, "traffic": None,
-        "kernel": "trace_rho_kernel", "algo_flops_per_point_step": ALGO_FLOPS[g.d],
+        "kernel": ("run_1d_kernel (persistent: all steps, trace + grid barrier + field tail)" if g.d == 1
+                   else f"trace_rho_kernel<{g.d}>"), "algo_flops_per_point_step": ALGO_FLOPS[g.d],
         "trace_launches": int(trace_launches), "trace_ms_per_launch": trace_ms / max(1, trace_launches),
         "trace_share_of_run": trace_ms / (trace_ms + reduce_ms + field_ms) if trace_ms else None,
         "peak_source": "measured in-run: DFMA-chain kernel (nufi_fp64_peak); MEASURED_PEAKS.json has no FP64 entry",
@@ -290,7 +292,7 @@ def gpu_arm(args, rank: int, world: int):
             "e2e": {"value": e2e_value, "unit": "point-steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": d2h,
                     "api": "Simulation(grid, ic, tau, N).run() -> host numpy rho/E/W/stats per time step"},
-            "gpu_launches": int(steps_per_run * 3),
+            "gpu_launches": launches_per_run * args.steps,
             "roofline": roofline,
             "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "clocks": clocks.summary(),

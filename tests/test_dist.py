@@ -1,0 +1,111 @@
+"""Multi-rank exchange logic on CPU ranks (gloo, world size 2).
+
+The GPU path (dist.DistributedSimulation) shards the velocity blocks, writes each
+rank's block sums into a zero-padded (B*Nx^d + 2B) table, SUM-allreduces it and
+runs the same fixed-order combine on every rank.  Here the per-block sums come
+from the oracle (test-only) so the sharding / exchange / combine logic runs on
+CPU: the combined rho must be bit-identical for world sizes 1 and 2, identical
+on every rank, and equal to the oracle's compute_rho to roundoff.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+from paper_2301_05581_b200.dist import ShardedStep, block_range
+
+B = 8
+
+
+def block_table(c, run, n, blocks):
+    """Zero-padded (B*nodes + 2B) table with the per-block v-sums of `blocks` (oracle)."""
+    nodes, cells = c.n_nodes, c.n_cells
+    per = cells // B
+    tab = np.zeros(B * nodes + 2 * B)
+    stack = run.stacked()[:n].reshape(n, -1) if n > 0 else None
+    X0 = O.x_node_matrix(c)
+    V0 = O.v_mid_matrix(c)
+    for b in blocks:
+        V = np.tile(V0[b * per:(b + 1) * per], (nodes, 1))
+        X = np.repeat(X0, per, axis=0)
+        if n > 0:
+            O.trace_backward(stack, c.L, n, c.tau, X, V, False)
+        F = O.eval_f0(c, X, V).reshape(nodes, per)
+        S = np.zeros(nodes)
+        for j in range(per):  # fixed order within the block
+            S = S + F[:, j]
+        tab[b * nodes:(b + 1) * nodes] = S
+        tab[B * nodes + 2 * b] = F.min()
+        tab[B * nodes + 2 * b + 1] = F.max()
+    return tab
+
+
+def sharded_rho(rank, world, name, steps):
+    c = O.case(name)
+    run = O.OracleRun(c)
+    out = []
+    lo, hi = block_range(B, rank, world)
+    st = ShardedStep(B=B, nodes=c.n_nodes)
+    for n in range(steps + 1):
+        t = torch.from_numpy(block_table(c, run, n, range(lo, hi)))
+        if world > 1:
+            dist.all_reduce(t)
+        rho, neut, fmn, fmx = st.combine(t.numpy(), run.rho_bar, c.hv ** c.d)
+        out.append(rho)
+        # advance the (oracle) history with the combined rho
+        phi, _ = O.solve_poisson(c, rho)
+        run.hist.append(O.fit_spline(c, phi))
+    return np.array(out)
+
+
+def _worker(rank, world, port, name, steps, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        q.put((rank, sharded_rho(rank, world, name, steps)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_block_range_covers_all_blocks():
+    for world in (1, 2, 4, 8):
+        seen = []
+        for r in range(world):
+            lo, hi = block_range(B, r, world)
+            seen += list(range(lo, hi))
+        assert seen == list(range(B))
+
+
+@pytest.mark.parametrize("name,steps", [("kat_wl", 6), ("tiny2", 3)])
+def test_two_rank_exchange_bit_identical(name, steps):
+    ref = sharded_rho(0, 1, name, steps)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, steps, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert np.array_equal(res[0], res[1]), "ranks disagree"
+    assert np.array_equal(res[0], ref), "world size changed the result"
+    # and the combine equals the oracle's compute_rho to roundoff
+    run = O.OracleRun(O.case(name)).run(steps)
+    scale = np.abs(run["rho"]).max(axis=1, keepdims=True)
+    assert (np.abs(ref - run["rho"]) / scale).max() < 1e-12

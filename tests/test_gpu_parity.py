@@ -168,7 +168,7 @@ def _check_run(name, g, sim, res, w_until=None, rho_tol=RHO_TOL):
     upto = N if w_until is None else w_until
     relW = np.abs(res.W[:upto] - g["W"][:upto]) / np.abs(g["W"][:upto])
     assert relW.max() <= W_TOL, (relW.argmax(), relW.max())
-    assert np.abs(res.stats[:N, 1:] - g["stats"][:N, 1:]).max() <= 1e-12 * max(1.0, np.abs(g["stats"][:, 2]).max())
+    assert np.abs(res.stats[:upto, 1:] - g["stats"][:upto, 1:]).max() <= 1e-12 * max(1.0, np.abs(g["stats"][:, 2]).max())
     return relW
 
 
