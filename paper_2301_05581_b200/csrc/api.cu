@@ -226,9 +226,13 @@ static void choose_tiling(nufi_handle *h) {
     if (h->d == 1) {
         warps = 8, ppt = 1, passes = 1;  // trace_rho_1d: one point per thread
     } else if (h->d == 2) {
-        warps = 8, ppt = 1, passes = 1;
+        warps = 8, ppt = 2, passes = 1;  // 2 interleaved points per thread, 2 CTAs / SM
     } else {
-        warps = 8, ppt = 1, passes = 4;
+        warps = 8, ppt = 2, passes = 4;
+    }
+    if (h->d >= 2) {
+        if (const char *e = getenv("NUFI_PPT")) ppt = std::max(1, std::min(2, atoi(e)));
+        if (const char *e = getenv("NUFI_PASSES")) passes = std::max(1, atoi(e));
     }
     while (warps > 1 && (per_block % (warps * ppt) != 0)) warps >>= 1;
     while (ppt > 1 && (per_block % (warps * ppt) != 0)) ppt >>= 1;
@@ -248,11 +252,18 @@ static void choose_tiling(nufi_handle *h) {
         h->stages = h->N >= 256 ? 2 : 4;  // 2 CTAs / SM for the large-N (throughput-bound) case
         if (const char *e = getenv("NUFI_D1_STAGES")) h->stages = std::max(2, atoi(e));
     } else if (h->d == 2) {
-        h->sps = std::max(1, 16384 / slab_bytes);
-        h->stages = 3;
+        h->sps = std::max(1, 40960 / slab_bytes);  // ~40 KB stages, 2-deep ring: 2 CTAs / SM
+        h->stages = 2;
     } else {
         h->sps = std::max(1, 32768 / slab_bytes);
         h->stages = 2;
+    }
+    if (h->d >= 2) {
+        if (const char *e = getenv("NUFI_SPS")) h->sps = std::max(1, atoi(e));
+        if (const char *e = getenv("NUFI_STAGES")) h->stages = std::max(2, atoi(e));
+        // keep the ring within the 227 KB per-CTA shared-memory limit
+        while (h->sps > 1 && (size_t)h->stages * h->sps * slab_bytes > 200 * 1024) --h->sps;
+        while (h->stages > 2 && (size_t)h->stages * h->sps * slab_bytes > 200 * 1024) --h->stages;
     }
 }
 

@@ -485,11 +485,8 @@ static __device__ __forceinline__ bool field_update_body(const FieldParams &p, d
             put(2 * N + i, K * g2);
         }
     } else {
-        const int row = N + 3, rows = nodes / N;
-        for (int e = threadIdx.x; e < rows * row; e += T) {
-            const int r = e / row, j = e % row;
-            put(e, evs * c[r * N + (j - 1 + N) % N]);
-        }
+        const int raw = ev_slab_raw_elems(d, N);
+        for (int e = threadIdx.x; e < raw; e += T) put(e, evs * c[ev_halo_source(d, N, e)]);
     }
     for (int e = ev_slab_raw_elems(d, N) + threadIdx.x; e < p.ev_slab_elems; e += T) put(e, 0.0);
     if (threadIdx.x == 0 && p.hist_len) *p.hist_len = p.slot + 1;

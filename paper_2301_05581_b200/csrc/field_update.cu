@@ -106,12 +106,8 @@ __global__ void build_ev_slabs_kernel(const double *__restrict__ hist, double *_
             ev[2 * N + i] = K * g2;
         }
     } else {
-        const int row = N + 3;
-        const int rows = nodes / N;
-        for (int e = threadIdx.x; e < rows * row; e += blockDim.x) {
-            const int r = e / row, j = e % row;
-            ev[e] = evs * c[r * N + (j - 1 + N) % N];
-        }
+        const int raw = ev_slab_raw_elems(d, N);
+        for (int e = threadIdx.x; e < raw; e += blockDim.x) ev[e] = evs * c[ev_halo_source(d, N, e)];
     }
     for (int e = ev_slab_raw_elems(d, N) + threadIdx.x; e < ev_slab_elems; e += blockDim.x) ev[e] = 0.0;
 }

@@ -17,9 +17,11 @@
 //   d = 1: three arrays [A | B | C] of N doubles: on cell i the kick is the
 //          quadratic A_i + fc*(B_i + fc*C_i)  (the B-spline derivative restricted
 //          to one cell, pre-multiplied by K);
-//   d = 2: [N][N+3]   raw coefficients, last axis with a periodic halo
-//          (halo index j' holds c[(j'-1) mod N]) so the 4 taps are contiguous;
-//   d = 3: [N][N][N+3] same halo on the last (z) axis.
+//   d = 2: [R][R], d = 3: [R][R][R] with R = N + 3: raw coefficients with a
+//          periodic halo on every axis (halo index j' holds c[(j' - 1) mod N]),
+//          so the 4^d stencil of the cell with lower corner i is the block at
+//          halo index i .. i+3 per axis: one base address + 4^d compile-time
+//          offsets, no per-tap index wrapping.
 #pragma once
 
 #include "nufi_internal.cuh"
@@ -27,7 +29,20 @@
 namespace nufi {
 
 __host__ __device__ constexpr int ev_slab_raw_elems(int d, int N) {
-    return d == 1 ? 3 * N : (d == 2 ? N * (N + 3) : N * N * (N + 3));
+    return d == 1 ? 3 * N : (d == 2 ? (N + 3) * (N + 3) : (N + 3) * (N + 3) * (N + 3));
+}
+
+// halo element e of a d >= 2 evaluation slab -> linear index of the raw slab
+__host__ __device__ inline int ev_halo_source(int d, int N, int e) {
+    const int R = N + 3;
+    int lin = 0;
+    int div = d == 2 ? R : R * R;
+    for (int a = 0; a < d; ++a) {
+        const int j = (e / div) % R;
+        lin = lin * N + (j - 1 + N) % N;
+        div /= R;
+    }
+    return lin;
 }
 // padded to a 16-byte multiple (TMA bulk copy granularity)
 __host__ __device__ constexpr int ev_slab_elems(int d, int N) {
@@ -43,9 +58,10 @@ __device__ __forceinline__ int wrap_idx(int i, int N) {
 
 // Kick through evaluation slab `slab` (smem or global): V += K * g(X), or half of
 // it (`half`: the tau/2 kicks of kernels.py:194-196 and 203-205).
-template <int D, bool POW2>
-__device__ __forceinline__ void kick(const double (&X)[D], double (&V)[D], const double *__restrict__ slab, int N,
+template <int D, bool POW2, int NX = 0>
+__device__ __forceinline__ void kick(const double (&X)[D], double (&V)[D], const double *__restrict__ slab, int N_,
                                      double K, bool half) {
+    const int N = NX ? NX : N_;  // compile-time N makes every stencil offset an immediate
     if constexpr (D == 1) {
         double fc;
         const int i = locate_centred<POW2>(X[0], N, fc);
@@ -54,18 +70,19 @@ __device__ __forceinline__ void kick(const double (&X)[D], double (&V)[D], const
         V[0] = half ? fma(0.5, kick, V[0]) : V[0] + kick;
         (void)K;
     } else if constexpr (D == 2) {
+        const int R = N + 3;
         double fx, fy;
         const int ix = locate_centred<POW2>(X[0], N, fx);
         const int iy = locate_centred<POW2>(X[1], N, fy);
         double wx[4], dwx[4], wy[4], dwy[4];
         bspline_w_dw(fx + 0.5, wx, dwx);
         bspline_w_dw(fy + 0.5, wy, dwy);
-        const int row = N + 3;
+        const double *c = slab + ix * R + iy;
         double gx = 0.0, gy = 0.0;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
-            const double *c = slab + wrap_idx<POW2>(ix - 1 + m, N) * row + iy;
-            const double c0 = c[0], c1 = c[1], c2 = c[2], c3 = c[3];
+            const double *cm = c + m * R;
+            const double c0 = cm[0], c1 = cm[1], c2 = cm[2], c3 = cm[3];
             const double r = fma(c3, wy[3], fma(c2, wy[2], fma(c1, wy[1], c0 * wy[0])));
             const double rd = fma(c3, dwy[3], fma(c2, dwy[2], fma(c1, dwy[1], c0 * dwy[0])));
             gx = fma(dwx[m], r, gx);
@@ -75,6 +92,7 @@ __device__ __forceinline__ void kick(const double (&X)[D], double (&V)[D], const
         V[0] = fma(k, gx, V[0]);
         V[1] = fma(k, gy, V[1]);
     } else {
+        const int R = N + 3;
         double fx, fy, fz;
         const int ix = locate_centred<POW2>(X[0], N, fx);
         const int iy = locate_centred<POW2>(X[1], N, fy);
@@ -83,16 +101,15 @@ __device__ __forceinline__ void kick(const double (&X)[D], double (&V)[D], const
         bspline_w_dw(fx + 0.5, wx, dwx);
         bspline_w_dw(fy + 0.5, wy, dwy);
         bspline_w_dw(fz + 0.5, wz, dwz);
-        const int row = N + 3;
+        const double *c = slab + (ix * R + iy) * R + iz;
         double gx = 0.0, gy = 0.0, gz = 0.0;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
-            const int xm = wrap_idx<POW2>(ix - 1 + m, N) * N;
             double sy = 0.0, sdy = 0.0, sdz = 0.0;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const double *c = slab + (xm + wrap_idx<POW2>(iy - 1 + q, N)) * row + iz;
-                const double c0 = c[0], c1 = c[1], c2 = c[2], c3 = c[3];
+                const double *cq = c + (m * R + q) * R;
+                const double c0 = cq[0], c1 = cq[1], c2 = cq[2], c3 = cq[3];
                 const double r = fma(c3, wz[3], fma(c2, wz[2], fma(c1, wz[1], c0 * wz[0])));
                 const double rd = fma(c3, dwz[3], fma(c2, dwz[2], fma(c1, dwz[1], c0 * dwz[0])));
                 sy = fma(wy[q], r, sy);
@@ -111,12 +128,12 @@ __device__ __forceinline__ void kick(const double (&X)[D], double (&V)[D], const
 }
 
 // One backward substep: drift x -= tau v, then kick through slab.
-template <int D, bool POW2>
+template <int D, bool POW2, int NX = 0>
 __device__ __forceinline__ void substep(double (&X)[D], double (&V)[D], const double *__restrict__ slab,
                                         int N, double K, bool half) {
 #pragma unroll
     for (int a = 0; a < D; ++a) X[a] -= V[a];
-    kick<D, POW2>(X, V, slab, N, K, half);
+    kick<D, POW2, NX>(X, V, slab, N, K, half);
 }
 
 }  // namespace nufi

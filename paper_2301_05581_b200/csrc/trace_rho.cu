@@ -23,8 +23,8 @@
 
 namespace nufi {
 
-template <int D, int PPT, bool POW2>
-__global__ void __launch_bounds__(512) trace_rho_kernel(const TraceRhoParams p, const double K) {
+template <int D, int PPT, bool POW2, int NX>
+__global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams p, const double K) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int warps = blockDim.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(512) trace_rho_kernel(const TraceRhoParams p, 
     double *ring = reinterpret_cast<double *>(smem_raw);
     uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)stages * sps * slab_elems);
     uint64_t *empty = full + stages;
-    double *red = reinterpret_cast<double *>(empty + stages);  // 3 * blockDim.x
+    double *red = ring;  // 3 * blockDim.x, aliases the ring once every stage is consumed
 
     const int tile = blockIdx.x % p.node_tiles;
     const int vt = p.vt_lo + blockIdx.x / p.node_tiles;
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(512) trace_rho_kernel(const TraceRhoParams p, 
             for (int k = k_hi; k >= k_lo; --k) {
                 const double *slab = buf + (size_t)(k - k_lo) * slab_elems;
 #pragma unroll
-                for (int pp = 0; pp < PPT; ++pp) substep<D, POW2>(X[pp], V[pp], slab, N, K, false);
+                for (int pp = 0; pp < PPT; ++pp) substep<D, POW2, NX>(X[pp], V[pp], slab, N, K, false);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(512) trace_rho_kernel(const TraceRhoParams p, 
 
     // fixed-order CTA reduction over warps (same v-tile, same node per lane)
     const int T = blockDim.x;
+    __syncthreads();  // every warp is done with the ring before it is reused as `red`
     red[threadIdx.x] = acc;
     red[T + threadIdx.x] = fmn;
     red[2 * T + threadIdx.x] = fmx;
@@ -233,14 +234,15 @@ __global__ void reduce_blocks_kernel(const double *__restrict__ partial, const d
 // ----------------------------------------------------------------------------
 
 size_t trace_rho_smem_bytes(const TraceRhoParams &p, int threads) {
-    return (size_t)p.stages * p.slabs_per_stage * p.ev_slab_elems * sizeof(double) +
-           2 * p.stages * sizeof(uint64_t) + 3 * (size_t)threads * sizeof(double);
+    const size_t ring = (size_t)p.stages * p.slabs_per_stage * p.ev_slab_elems * sizeof(double);
+    const size_t red = 3 * (size_t)threads * sizeof(double);
+    return (ring > red ? ring : red) + 2 * p.stages * sizeof(uint64_t);
 }
 
-template <int D, int PPT, bool POW2>
+template <int D, int PPT, bool POW2, int NX>
 static cudaError_t launch_one(const TraceRhoParams &p, double K, int ctas, int threads, size_t smem,
                               cudaStream_t st) {
-    auto kern = trace_rho_kernel<D, PPT, POW2>;
+    auto kern = trace_rho_kernel<D, PPT, POW2, NX>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<ctas, threads, smem, st>>>(p, K);
@@ -251,9 +253,13 @@ cudaError_t launch_trace_rho(int d, int ppt, bool pow2, const TraceRhoParams &p,
                              cudaStream_t st) {
     const size_t smem = trace_rho_smem_bytes(p, threads);
 #define NUFI_TR(DD, PP)                                                                              \
-    if (d == DD && ppt == PP)                                                                        \
-        return pow2 ? launch_one<DD, PP, true>(p, K, ctas, threads, smem, st)                        \
-                    : launch_one<DD, PP, false>(p, K, ctas, threads, smem, st);
+    if (d == DD && ppt == PP) {                                                                      \
+        if (p.N == 8) return launch_one<DD, PP, true, 8>(p, K, ctas, threads, smem, st);             \
+        if (p.N == 16) return launch_one<DD, PP, true, 16>(p, K, ctas, threads, smem, st);           \
+        if (p.N == 32) return launch_one<DD, PP, true, 32>(p, K, ctas, threads, smem, st);           \
+        return pow2 ? launch_one<DD, PP, true, 0>(p, K, ctas, threads, smem, st)                     \
+                    : launch_one<DD, PP, false, 0>(p, K, ctas, threads, smem, st);                   \
+    }
     NUFI_TR(2, 1)
     NUFI_TR(3, 1)
     NUFI_TR(2, 2)
