@@ -37,6 +37,10 @@ extern "C" {
 
 #define NUFI_MAX_CENTERS 4
 
+/* nufi_config.flags */
+#define NUFI_FLAG_F32_HISTORY 1 /* PotentialHistory(dtype=float32), spline.py:118-125: every stored
+                                   coefficient is rounded to float32 (the trace reads it as double) */
+
 /* nufi_trace modes */
 #define NUFI_TRACE_FAST 0   /* production arithmetic (FMA, cell-centred polynomial form) */
 #define NUFI_TRACE_PARITY 1 /* reference operation order, no FMA: bit-exact vs kernels.py */
@@ -71,7 +75,7 @@ typedef struct nufi_config {
     int32_t v_blocks;
     int32_t block_lo;
     int32_t block_hi;
-    int32_t flags; /* reserved, 0 */
+    int32_t flags; /* NUFI_FLAG_* */
 } nufi_config;
 
 typedef struct nufi_handle nufi_handle;
@@ -163,6 +167,18 @@ int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, d
  * evals (optional) += M * (n + half_kick) for n > 0. */
 int nufi_trace(nufi_handle *h, int64_t n, double *X, double *V, int64_t M, int half_kick, int mode,
                int64_t *evals);
+
+/* Observable sweep at step n (density.quadrature_sweep_many, density.py:94-120,
+ * for the conserved-quantity weights of SPEC.md:403-406): every quadrature
+ * point of this handle's velocity blocks is traced with Psi (needs len >= n+1
+ * for n > 0, else NUFI_ERR_USAGE like flow.py:106-112), f = f0(foot), and
+ *   out[0] = hx^d hv^d sum f          out[1] = hx^d hv^d sum f^2
+ *   out[2] = hx^d hv^d sum f ln f     out[3] = hx^d hv^d sum |v|^2 f / 2
+ *   out[4 + a] = hx^d hv^d sum v_a f  (a < d)
+ *   out[4 + d] = min f,  out[5 + d] = max f
+ * with weights taken at the untraced quadrature point (density.py:57-60).
+ * out: 6 + d doubles.  evals (optional) += points * (n + 1) for n > 0. */
+int nufi_moments(nufi_handle *h, int64_t n, double *out, int64_t *evals);
 
 /* f0 at caller points (eval_f0, initial.py:165-180): F[M]. */
 int nufi_eval_f0(nufi_handle *h, const double *X, const double *V, int64_t M, double *F);

@@ -82,6 +82,8 @@ FOUR_PI = 4.0 * math.pi
 
 
 def case(name: str) -> Case:
+    if name.endswith("_f32"):  # FP32 history variants: same case, OracleRun(..., f32=True)
+        return case(name[: -len("_f32")])
     if name == "wl1":
         return Case(1, FOUR_PI, 64, 256, 6.0, 1 / 8, 0.01, 0.5, (_MAX,))
     if name == "ts1":
@@ -389,8 +391,9 @@ def fit_spline(c: Case, phi: np.ndarray) -> np.ndarray:
 class OracleRun:
     """The canonical loop: compute_rho -> solve_poisson -> fit_spline -> append."""
 
-    def __init__(self, c: Case, threads: int = 0, chunk: int = DEFAULT_CHUNK):
+    def __init__(self, c: Case, threads: int = 0, chunk: int = DEFAULT_CHUNK, f32: bool = False):
         self.c = c
+        self.f32 = f32  # PotentialHistory(dtype=float32): append casts the slab (spline.py:118-125, 140)
         self.threads = threads
         self.chunk = chunk
         self.rho_bar = background_density(c)
@@ -438,16 +441,45 @@ class OracleRun:
         rho -= constant
         return rho, constant, f_min, f_max
 
+    def quadrature_sweep_many(self, n: int, weights, stack=None):
+        """density.py:104-120: Psi-traced (half kick, flow.py:106-112) node-aligned
+        batches, weights at the untraced points (density.py:45-61), per-batch
+        np.add.reduce, total times hx^d hv^d.  stack: (rows, Nx^d) history
+        (default: this run's), needs rows >= n + 1 for n > 0."""
+        c = self.c
+        stack = self.stacked().reshape(len(self.hist), -1) if stack is None else np.asarray(stack)
+        stack = stack.reshape(stack.shape[0], -1)
+        if n > 0 and stack.shape[0] < n + 1:
+            raise ValueError("history too short for psi")
+        n_cells = c.n_cells
+        nodes_per = max(1, self.chunk // n_cells)
+        totals = [None] * len(weights)
+        for start in range(0, c.n_nodes, nodes_per):
+            stop = min(start + nodes_per, c.n_nodes)
+            Xb = np.repeat(self._X[start:stop], n_cells, axis=0)
+            Vb = np.tile(self._V, (stop - start, 1))
+            Xt, Vt = Xb.copy(), Vb.copy()
+            if n > 0:
+                self.field_evals += trace_backward(np.ascontiguousarray(stack[: n + 1]), c.L, n, c.tau, Xt, Vt,
+                                                   True, self.threads)
+            F = eval_f0(c, Xt, Vt)
+            for iw, w in enumerate(weights):
+                part = np.add.reduce(np.asarray(w(Xb, Vb, F), dtype=np.float64), axis=0)
+                totals[iw] = part if totals[iw] is None else totals[iw] + part
+        measure = c.hx ** c.d * c.hv ** c.d
+        return [t * measure for t in totals]
+
     def step(self, n: int):
         """One full step n; returns dict(rho, coeffs, E, W, stats)."""
         c = self.c
         rho, neut, fmin, fmax = self.compute_rho(n)
         phi, phi_hat = solve_poisson(c, rho)
         coeffs = fit_spline(c, phi)
-        self.hist.append(coeffs)
+        stored = coeffs.astype(np.float32).astype(np.float64) if self.f32 else coeffs
+        self.hist.append(stored)
         W = electric_energy(c, phi_hat)
         E = eval_E_many(coeffs, c.L, self._X)
-        return dict(rho=rho, coeffs=coeffs.reshape(-1), E=E, W=W, stats=(neut, fmin, fmax))
+        return dict(rho=rho, coeffs=stored.reshape(-1), E=E, W=W, stats=(neut, fmin, fmax))
 
     def run(self, N: int, keep: int | None = None):
         keep = N + 1 if keep is None else keep
@@ -461,6 +493,16 @@ class OracleRun:
                 out["coeffs"].append(s["coeffs"])
                 out["E"].append(s["E"])
         return {k: np.array(v) for k, v in out.items()}
+
+
+def conserved_weights():
+    """SPEC.md:403-406 weights: f, f^2, f ln f (0 ln 0 := 0), |v|^2 f / 2, v f."""
+
+    def f_ln_f(X, V, F):
+        return np.where(F > 0, F * np.log(np.where(F > 0, F, 1.0)), 0.0)
+
+    return [lambda X, V, F: F, lambda X, V, F: F * F, f_ln_f,
+            lambda X, V, F: 0.5 * np.sum(V * V, axis=1) * F, lambda X, V, F: V * F[:, None]]
 
 
 def point_steps(c: Case, N: int) -> int:

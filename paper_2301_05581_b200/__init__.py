@@ -7,7 +7,9 @@ rho, plus the per-step Poisson / spline append — in hand-written sm_100a CUDA
 module names: grids, initial, spline, flow, density, driver.
 """
 
-from .density import DEFAULT_CHUNK, DensityGrid, RhoResult, compute_rho
+from .density import (DEFAULT_CHUNK, ConservedMoments, DensityGrid, RhoResult, compute_rho, conserved_moments,
+                      quadrature_sweep, quadrature_sweep_many)
+from .diagnostics import DiagnosticsRecord, conserved_quantities, electric_energy_from_coeffs, fit_damping_rate
 from .driver import FieldUpdate, RunResult, Simulation, StepOutput, advance, point_steps, run_simulation
 from .errors import ConfigError, FitError, NumericalConsistencyError, UsageError, VpflowError
 from .flow import (TRACE_FAST, TRACE_PARITY, FlowContext, eval_f, eval_f0, eval_f_batch, psi, psi_batch,

@@ -25,6 +25,7 @@ NUFI_ERR_COMM = 5
 NUFI_MAX_CENTERS = 4
 NUFI_TRACE_FAST = 0
 NUFI_TRACE_PARITY = 1
+NUFI_FLAG_F32_HISTORY = 1
 
 
 class CudaError(VpflowError):
@@ -95,6 +96,7 @@ _SIGS = {
     "nufi_run": [_P, _I64, _P, _P, _P, _P, _I64P],
     "nufi_trace": [_P, _I64, _P, _P, _I64, ctypes.c_int, ctypes.c_int, _I64P],
     "nufi_eval_f0": [_P, _P, _P, _I64, _P],
+    "nufi_moments": [_P, _I64, _P, _I64P],
     "nufi_profiling": [_P, ctypes.c_int],
     "nufi_profiling_read": [_P, _P],
     "nufi_fp64_peak": [ctypes.c_int, ctypes.POINTER(_D), ctypes.POINTER(_D)],
@@ -139,7 +141,7 @@ def check(rc: int) -> None:
 
 
 def make_config(grid, ic, tau: float, n_max: int, rho_bar: float | None = None, v_blocks: int = 0,
-                block_lo: int = 0, block_hi: int = 0) -> NufiConfig:
+                block_lo: int = 0, block_hi: int = 0, flags: int = 0) -> NufiConfig:
     c = NufiConfig()
     c.d = grid.d
     c.Nx = grid.Nx
@@ -162,7 +164,7 @@ def make_config(grid, ic, tau: float, n_max: int, rho_bar: float | None = None, 
     c.v_blocks = int(v_blocks)
     c.block_lo = int(block_lo)
     c.block_hi = int(block_hi)
-    c.flags = 0
+    c.flags = int(flags)
     return c
 
 

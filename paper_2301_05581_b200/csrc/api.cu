@@ -19,6 +19,9 @@ namespace nufi {
 size_t trace_rho_smem_bytes(const TraceRhoParams &p, int threads);
 cudaError_t launch_trace_rho(int d, int ppt, bool pow2, const TraceRhoParams &p, double K, int ctas, int threads,
                              cudaStream_t st);
+cudaError_t launch_sweep_moments(int d, int ppt, bool pow2, const TraceRhoParams &p, double K, int ctas, int threads,
+                                 cudaStream_t st);
+cudaError_t launch_reduce_moments(const double *part, int rows, int d, double measure, double *out, cudaStream_t st);
 cudaError_t launch_reduce_blocks(const double *partial, const double *fminmax, double *out, int nodes,
                                  int node_tiles, int vt_per_block, int b_lo, int b_hi, int B, cudaStream_t st);
 cudaError_t launch_trace_points(int d, int mode, bool pow2, const double *hist, const double *ev_hist,
@@ -41,8 +44,8 @@ struct Run1DParams {
     unsigned long long *stamps;
 };
 cudaError_t launch_run_1d(const Run1DParams &P, int threads, int device, cudaStream_t st, int *grid_out);
-cudaError_t launch_build_ev_slabs(const double *hist, double *ev_hist, int d, int N, int nodes, int ev_slab_elems,
-                                  double K, int64_t r0, int64_t r1, cudaStream_t st);
+cudaError_t launch_build_ev_slabs(double *hist, double *ev_hist, int d, int N, int nodes, int ev_slab_elems,
+                                  double K, int64_t r0, int64_t r1, int f32, cudaStream_t st);
 }  // namespace nufi
 
 namespace nufi {
@@ -110,8 +113,11 @@ struct nufi_handle {
     // run outputs (device) and their pinned host staging
     double *run_dev = nullptr, *run_host = nullptr;
     size_t run_elems = 0;
+    // observable sweep: per-CTA moment rows + the reduced vector (lazily allocated)
+    double *mom_part = nullptr, *d_mom = nullptr;
 
     int64_t len = 0;  // host mirror of the history length
+    int f32 = 0;      // NUFI_FLAG_F32_HISTORY
 
     // optional per-launch event timing (nufi_profile)
     bool profiling = false;
@@ -185,6 +191,7 @@ static int validate(const nufi_config &c) {
         return fail(NUFI_ERR_USAGE, buf);
     }
     if (c.n_max < 0) return fail(NUFI_ERR_USAGE, "n_max must be >= 0");
+    if (c.flags & ~NUFI_FLAG_F32_HISTORY) return fail(NUFI_ERR_USAGE, "unknown nufi_config flags");
     for (int a = 0; a < c.d; ++a) {
         const nufi_profile &p = c.profiles[a];
         if (p.n_centers < 1 || p.n_centers > NUFI_MAX_CENTERS)
@@ -410,6 +417,7 @@ int nufi_create(const nufi_config *cfg, int device, void *stream, nufi_handle **
         return fail(NUFI_ERR_USAGE, "block range outside [0, v_blocks)");
     }
     h->ev_elems = ev_slab_elems(c.d, c.Nx);
+    h->f32 = (c.flags & NUFI_FLAG_F32_HISTORY) ? 1 : 0;
     choose_tiling(h);
 
     const size_t nodes = h->nodes;
@@ -450,7 +458,7 @@ int nufi_destroy(nufi_handle *h) {
     for (void *p : {(void *)h->hist, (void *)h->ev_hist, (void *)h->partial, (void *)h->fminmax, (void *)h->blocks,
                     (void *)h->d_rho, (void *)h->d_E, (void *)h->d_W, (void *)h->d_stats, (void *)h->d_rho_bar,
                     (void *)h->d_status, (void *)h->d_len, (void *)h->run_dev, (void *)h->tables,
-                    (void *)h->ticket, (void *)h->barrier})
+                    (void *)h->ticket, (void *)h->barrier, (void *)h->mom_part, (void *)h->d_mom})
         if (p) cudaFree(p);
     if (h->run_host) cudaFreeHost(h->run_host);
     if (h->own_stream) cudaStreamDestroy(h->stream);
@@ -486,7 +494,8 @@ int nufi_load_history(nufi_handle *h, const double *coeffs, int64_t count) {
     if (count > 0 && !coeffs) return fail(NUFI_ERR_USAGE, "null coefficients");
     if (count > 0) {
         CU(cudaMemcpyAsync(h->hist, coeffs, (size_t)count * h->nodes * sizeof(double), cudaMemcpyDefault, h->stream));
-        CU(launch_build_ev_slabs(h->hist, h->ev_hist, h->d, h->N, h->nodes, h->ev_elems, h->K, 0, count, h->stream));
+        CU(launch_build_ev_slabs(h->hist, h->ev_hist, h->d, h->N, h->nodes, h->ev_elems, h->K, 0, count, h->f32,
+                                 h->stream));
     }
     h->len = count;
     CU(cudaMemcpyAsync(h->d_len, &h->len, sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
@@ -512,7 +521,7 @@ int nufi_append_coeffs(nufi_handle *h, const double *coeffs) {
     CU(cudaMemcpyAsync(h->hist + (size_t)h->len * h->nodes, coeffs, (size_t)h->nodes * sizeof(double),
                        cudaMemcpyDefault, h->stream));
     CU(launch_build_ev_slabs(h->hist, h->ev_hist, h->d, h->N, h->nodes, h->ev_elems, h->K, h->len, h->len + 1,
-                             h->stream));
+                             h->f32, h->stream));
     h->len += 1;
     CU(cudaStreamSynchronize(h->stream));
     return NUFI_OK;
@@ -581,6 +590,7 @@ static FieldParams field_params(nufi_handle *h) {
     f.ev_slab_elems = h->ev_elems;
     f.status = h->d_status;
     f.hist_len = h->d_len;
+    f.f32_hist = h->f32;
     return f;
 }
 
@@ -978,6 +988,40 @@ int nufi_trace(nufi_handle *h, int64_t n, double *X, double *V, int64_t M, int h
     if (!dv) CU(cudaFreeAsync(dV, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     if (evals) *evals += M * need;
+    return NUFI_OK;
+}
+
+int nufi_moments(nufi_handle *h, int64_t n, double *out, int64_t *evals) {
+    CHECK_HANDLE(h);
+    if (n < 0) return fail(NUFI_ERR_USAGE, "step index must be >= 0");
+    if (!out) return fail(NUFI_ERR_USAGE, "null output");
+    if (n > 0 && h->len < n + 1) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "psi at step %lld needs fields 0..%lld; history holds %lld", (long long)n,
+                 (long long)n, (long long)h->len);  // flow.py:55-62, 106-112
+        return fail(NUFI_ERR_USAGE, buf);
+    }
+    const int nm = mom_sums(h->d) + 2;
+    const int ctas = (h->b_hi - h->b_lo) * h->vt_per_block * h->node_tiles;
+    if (!h->mom_part) {
+        CU(cudaMalloc(&h->mom_part, (size_t)h->vt_total * h->node_tiles * nm * sizeof(double)));
+        CU(cudaMalloc(&h->d_mom, 16 * sizeof(double)));
+    }
+    TraceRhoParams p = trace_params(h, n, h->b_lo);
+    p.partial = h->mom_part;
+    // one point per thread for the sweep (the extra moment accumulators would
+    // spill the 2-point d = 3 variant); the same rows in twice the passes
+    const int ppt = 1;
+    p.passes = h->passes * h->ppt;
+    const double measure = std::pow(h->hx, (double)h->d) * h->hv_d;  // density.py:107
+    {
+        ProfScope ps(h, 0, point_steps(h, n > 0 ? n + 1 : 0, h->b_hi - h->b_lo));
+        CU(launch_sweep_moments(h->d, ppt, h->pow2, p, h->K, ctas, h->threads, h->stream));
+    }
+    CU(launch_reduce_moments(h->mom_part, ctas, h->d, measure, h->d_mom, h->stream));
+    CU(cudaMemcpyAsync(out, h->d_mom, nm * sizeof(double), cudaMemcpyDefault, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    if (evals && n > 0) *evals += (int64_t)point_steps(h, n + 1, h->b_hi - h->b_lo);
     return NUFI_OK;
 }
 

@@ -56,6 +56,7 @@ struct FieldParams {
     int *status;        // NUFI_ERR_NUMERICAL when rho is not neutral
     int64_t *hist_len;  // device-side history length (slot + 1)
     int finish_only;    // compute_rho only: stop after rho / stats
+    int f32_hist;       // FP32 history (spline.py:118-125): stored slabs rounded to float
     unsigned long long *tstamps;  // debug: phase timestamps (thread 0), 10 slots
 };
 
@@ -73,6 +74,10 @@ struct FieldParams {
 __host__ __device__ constexpr int field_smem_doubles(int nodes, int N, bool staged) {
     return 4 * nodes + 2 * N + (staged ? 8 * nodes : 0) + 64;
 }
+
+// FP32 history mode: a stored coefficient is the float32 rounding of the fit
+// (PotentialHistory(dtype=float32) casts on append, spline.py:140), read back as double.
+__device__ __forceinline__ double hist_round(double c, int f32) { return f32 ? (double)__double2float_rn(c) : c; }
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -290,7 +295,10 @@ static __device__ __forceinline__ bool field_update_1d_body(const FieldParams &p
     double *evl = p.ev_local;
     double *hrow = p.hist ? p.hist + (size_t)p.slot * N : nullptr;
     for (int i = threadIdx.x; i < N; i += T) {
-        const double c0 = c[(i - 1 + N) & (N - 1)], c1 = c[i], c2 = c[(i + 1) & (N - 1)], c3 = c[(i + 2) & (N - 1)];
+        const double e0 = c[(i - 1 + N) & (N - 1)], e1 = c[i], e2 = c[(i + 1) & (N - 1)], e3 = c[(i + 2) & (N - 1)];
+        // the stored (and traced) slab; E at the nodes comes from the fit itself
+        const double c0 = hist_round(e0, p.f32_hist), c1 = hist_round(e1, p.f32_hist),
+                     c2 = hist_round(e2, p.f32_hist), c3 = hist_round(e3, p.f32_hist);
         const double g0 = 0.5 * (c2 - c0);
         const double g1 = (c0 - 2.0 * c1) + c2;
         const double g2 = (1.5 * (c1 - c2)) + 0.5 * (c3 - c0);
@@ -309,7 +317,7 @@ static __device__ __forceinline__ bool field_update_1d_body(const FieldParams &p
         if (hrow) hrow[i] = c1;
         if (p.coeffs_out) p.coeffs_out[i] = c1;
         // E(x_i) = -(N/L) (-c_{i-1}/2 + c_{i+1}/2)  (f = 0 stencil, kernels.py:102-123)
-        if (p.E_out) p.E_out[i] = -(0.5 * (c2 - c0)) * p.inv_h;
+        if (p.E_out) p.E_out[i] = -(0.5 * (e2 - e0)) * p.inv_h;
     }
     if (threadIdx.x == 0) {
         for (int e = 3 * N; e < p.ev_slab_elems; ++e) {
@@ -461,8 +469,8 @@ static __device__ __forceinline__ bool field_update_body(const FieldParams &p, d
     if (p.hist) {
         double *hrow = p.hist + (size_t)p.slot * nodes;
         for (int i = threadIdx.x; i < nodes; i += T) {
-            hrow[i] = c[i];
-            if (p.coeffs_out) p.coeffs_out[i] = c[i];
+            hrow[i] = hist_round(c[i], p.f32_hist);
+            if (p.coeffs_out) p.coeffs_out[i] = hrow[i];
         }
     }
     double *evg = p.ev_hist ? p.ev_hist + (size_t)p.slot * p.ev_slab_elems : nullptr;
@@ -475,7 +483,8 @@ static __device__ __forceinline__ bool field_update_body(const FieldParams &p, d
     const double evs = p.slot == 0 ? 0.5 : 1.0;
     if (d == 1) {
         for (int i = threadIdx.x; i < N; i += T) {
-            const double c0 = c[(i - 1 + N) % N], c1 = c[i], c2 = c[(i + 1) % N], c3 = c[(i + 2) % N];
+            const double c0 = hist_round(c[(i - 1 + N) % N], p.f32_hist), c1 = hist_round(c[i], p.f32_hist),
+                         c2 = hist_round(c[(i + 1) % N], p.f32_hist), c3 = hist_round(c[(i + 2) % N], p.f32_hist);
             const double g0 = 0.5 * (c2 - c0);
             const double g1 = (c0 - 2.0 * c1) + c2;
             const double g2 = (1.5 * (c1 - c2)) + 0.5 * (c3 - c0);
@@ -486,7 +495,7 @@ static __device__ __forceinline__ bool field_update_body(const FieldParams &p, d
         }
     } else {
         const int raw = ev_slab_raw_elems(d, N);
-        for (int e = threadIdx.x; e < raw; e += T) put(e, evs * c[ev_halo_source(d, N, e)]);
+        for (int e = threadIdx.x; e < raw; e += T) put(e, evs * hist_round(c[ev_halo_source(d, N, e)], p.f32_hist));
     }
     for (int e = ev_slab_raw_elems(d, N) + threadIdx.x; e < p.ev_slab_elems; e += T) put(e, 0.0);
     if (threadIdx.x == 0 && p.hist_len) *p.hist_len = p.slot + 1;

@@ -88,10 +88,15 @@ cudaError_t launch_field_tables(double *tw, double *fac, double *k2, int d, int 
 }
 
 // Evaluation slabs (trace_common.cuh layouts) for raw rows [r0, r1) of hist.
-__global__ void build_ev_slabs_kernel(const double *__restrict__ hist, double *__restrict__ ev_hist, int d, int N,
-                                      int nodes, int ev_slab_elems, double K, int64_t r0) {
+// f32: FP32 history mode -- round the raw row in place first (spline.py:118-125, 140).
+__global__ void build_ev_slabs_kernel(double *__restrict__ hist, double *__restrict__ ev_hist, int d, int N,
+                                      int nodes, int ev_slab_elems, double K, int64_t r0, int f32) {
     const int64_t slot = r0 + blockIdx.x;
-    const double *c = hist + (size_t)slot * nodes;
+    double *c = hist + (size_t)slot * nodes;
+    if (f32) {
+        for (int i = threadIdx.x; i < nodes; i += blockDim.x) c[i] = hist_round(c[i], 1);
+        __syncthreads();
+    }
     double *ev = ev_hist + (size_t)slot * ev_slab_elems;
     const double evs = slot == 0 ? 0.5 : 1.0;  // slab 0 stored pre-halved (field_common.cuh)
     if (d == 1) {
@@ -112,10 +117,10 @@ __global__ void build_ev_slabs_kernel(const double *__restrict__ hist, double *_
     for (int e = ev_slab_raw_elems(d, N) + threadIdx.x; e < ev_slab_elems; e += blockDim.x) ev[e] = 0.0;
 }
 
-cudaError_t launch_build_ev_slabs(const double *hist, double *ev_hist, int d, int N, int nodes, int ev_slab_elems,
-                                  double K, int64_t r0, int64_t r1, cudaStream_t st) {
+cudaError_t launch_build_ev_slabs(double *hist, double *ev_hist, int d, int N, int nodes, int ev_slab_elems,
+                                  double K, int64_t r0, int64_t r1, int f32, cudaStream_t st) {
     if (r1 <= r0) return cudaSuccess;
-    build_ev_slabs_kernel<<<(unsigned)(r1 - r0), 256, 0, st>>>(hist, ev_hist, d, N, nodes, ev_slab_elems, K, r0);
+    build_ev_slabs_kernel<<<(unsigned)(r1 - r0), 256, 0, st>>>(hist, ev_hist, d, N, nodes, ev_slab_elems, K, r0, f32);
     return cudaGetLastError();
 }
 

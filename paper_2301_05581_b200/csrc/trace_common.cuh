@@ -44,6 +44,9 @@ __host__ __device__ inline int ev_halo_source(int d, int N, int e) {
     }
     return lin;
 }
+// conserved-quantity sweep: sums f, f^2, f ln f, |v|^2 f / 2, v_a f (then f_min, f_max)
+__host__ __device__ constexpr int mom_sums(int d) { return 4 + d; }
+
 // padded to a 16-byte multiple (TMA bulk copy granularity)
 __host__ __device__ constexpr int ev_slab_elems(int d, int N) {
     return (ev_slab_raw_elems(d, N) + 1) & ~1;

@@ -23,7 +23,13 @@
 
 namespace nufi {
 
-template <int D, int PPT, bool POW2, int NX>
+// MOM = false: compute_rho (Psi-tilde, per-node v-sums).
+// MOM = true:  the observable sweep of density.quadrature_sweep_many
+// (density.py:94-120) for the fixed conserved-quantity weights: Psi (leading
+// half kick through slab n, kernels.py:194-196), f = f0(foot), and per-CTA sums
+// of f, f^2, f ln f, |v|^2 f / 2, v_a f at the UNTRACED quadrature point plus
+// (f_min, f_max) -> p.partial[cta][mom_count(D)].
+template <int D, int PPT, bool POW2, int NX, bool MOM>
 __global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams p, const double K) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int warps = blockDim.x >> 5;
@@ -83,6 +89,10 @@ __global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams 
     }
 
     double acc = 0.0, fmn = DBL_MAX, fmx = -DBL_MAX;
+    constexpr int NS = MOM ? mom_sums(D) : 1;
+    double mom[NS];
+#pragma unroll
+    for (int q = 0; q < NS; ++q) mom[q] = 0.0;
     int it = 0;
     for (int pass = 0; pass < p.passes; ++pass) {
         double X[PPT][D], V[PPT][D];
@@ -100,6 +110,8 @@ __global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams 
                 X[pp][a] = (double)ni[a] - 0.5;
                 V[pp][a] = v * p.vel_to_scaled;
             }
+            // Psi's leading half kick through the step's own field (slab n, read in place)
+            if (MOM && n >= 1) kick<D, POW2, NX>(X[pp], V[pp], p.ev_hist + (size_t)n * slab_elems, N, K, true);
         }
 
         for (int st = 0; st < stages_per_pass; ++st, ++it) {
@@ -144,11 +156,60 @@ __global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams 
             }
             const double f = eval_f0<D>(p.f0, x, v);
             if (valid) {
-                acc += f;
                 fmn = fmin(fmn, f);
                 fmx = fmax(fmx, f);
+                if constexpr (MOM) {
+                    // weights at the untraced point (density.py:57-60): v0 of row jrow
+                    double v0[D], v2 = 0.0;
+                    int64_t r = jrow[pp];
+#pragma unroll
+                    for (int a = D - 1; a >= 0; --a) {
+                        v0[a] = __dadd_rn(-p.vmax, __dmul_rn((double)(int)(r % p.Nv) + 0.5, p.hv));
+                        r /= p.Nv;
+                    }
+#pragma unroll
+                    for (int a = 0; a < D; ++a) v2 = fma(v0[a], v0[a], v2);
+                    mom[0] += f;
+                    mom[1] = fma(f, f, mom[1]);
+                    mom[2] += f > 0.0 ? f * log(f) : 0.0;  // 0 ln 0 := 0 (SPEC diagnostics)
+                    mom[3] = fma(0.5 * v2, f, mom[3]);
+#pragma unroll
+                    for (int a = 0; a < D; ++a) mom[4 + a] = fma(v0[a], f, mom[4 + a]);
+                } else {
+                    acc += f;
+                }
             }
         }
+    }
+
+    if constexpr (MOM) {
+        // fixed-order CTA reduction of the moment sums and (min, max)
+        constexpr int NM = NS + 2;
+        const int T = blockDim.x;
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < NS; ++q) red[q * T + threadIdx.x] = mom[q];
+        red[NS * T + threadIdx.x] = fmn;
+        red[(NS + 1) * T + threadIdx.x] = fmx;
+        __syncthreads();
+        if (warp == 0) {
+            double* out = p.partial + (size_t)blockIdx.x * NM;
+#pragma unroll
+            for (int q = 0; q < NM; ++q) {
+                double s = q < NS ? 0.0 : (q == NS ? DBL_MAX : -DBL_MAX);
+                for (int w = 0; w < warps; ++w) {
+                    const double x = red[q * T + w * 32 + lane];
+                    s = q < NS ? s + x : (q == NS ? fmin(s, x) : fmax(s, x));
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double y = __shfl_xor_sync(0xffffffffu, s, o);
+                    s = q < NS ? s + y : (q == NS ? fmin(s, y) : fmax(s, y));
+                }
+                if (lane == 0) out[q] = s;
+            }
+        }
+        return;
     }
 
     // fixed-order CTA reduction over warps (same v-tile, same node per lane)
@@ -235,14 +296,14 @@ __global__ void reduce_blocks_kernel(const double *__restrict__ partial, const d
 
 size_t trace_rho_smem_bytes(const TraceRhoParams &p, int threads) {
     const size_t ring = (size_t)p.stages * p.slabs_per_stage * p.ev_slab_elems * sizeof(double);
-    const size_t red = 3 * (size_t)threads * sizeof(double);
+    const size_t red = (size_t)(mom_sums(3) + 2) * (size_t)threads * sizeof(double);
     return (ring > red ? ring : red) + 2 * p.stages * sizeof(uint64_t);
 }
 
-template <int D, int PPT, bool POW2, int NX>
+template <int D, int PPT, bool POW2, int NX, bool MOM = false>
 static cudaError_t launch_one(const TraceRhoParams &p, double K, int ctas, int threads, size_t smem,
                               cudaStream_t st) {
-    auto kern = trace_rho_kernel<D, PPT, POW2, NX>;
+    auto kern = trace_rho_kernel<D, PPT, POW2, NX, MOM>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<ctas, threads, smem, st>>>(p, K);
@@ -254,11 +315,11 @@ cudaError_t launch_trace_rho(int d, int ppt, bool pow2, const TraceRhoParams &p,
     const size_t smem = trace_rho_smem_bytes(p, threads);
 #define NUFI_TR(DD, PP)                                                                              \
     if (d == DD && ppt == PP) {                                                                      \
-        if (p.N == 8) return launch_one<DD, PP, true, 8>(p, K, ctas, threads, smem, st);             \
-        if (p.N == 16) return launch_one<DD, PP, true, 16>(p, K, ctas, threads, smem, st);           \
-        if (p.N == 32) return launch_one<DD, PP, true, 32>(p, K, ctas, threads, smem, st);           \
-        return pow2 ? launch_one<DD, PP, true, 0>(p, K, ctas, threads, smem, st)                     \
-                    : launch_one<DD, PP, false, 0>(p, K, ctas, threads, smem, st);                   \
+        if (p.N == 8) return launch_one<DD, PP, true, 8, false>(p, K, ctas, threads, smem, st);             \
+        if (p.N == 16) return launch_one<DD, PP, true, 16, false>(p, K, ctas, threads, smem, st);           \
+        if (p.N == 32) return launch_one<DD, PP, true, 32, false>(p, K, ctas, threads, smem, st);           \
+        return pow2 ? launch_one<DD, PP, true, 0, false>(p, K, ctas, threads, smem, st)                     \
+                    : launch_one<DD, PP, false, 0, false>(p, K, ctas, threads, smem, st);                   \
     }
     NUFI_TR(2, 1)
     NUFI_TR(3, 1)
@@ -266,6 +327,57 @@ cudaError_t launch_trace_rho(int d, int ppt, bool pow2, const TraceRhoParams &p,
     NUFI_TR(3, 2)
 #undef NUFI_TR
     return cudaErrorInvalidValue;
+}
+
+// Observable sweep (MOM = true): one CTA per tile, outputs p.partial[cta][mom_count(d)].
+cudaError_t launch_sweep_moments(int d, int ppt, bool pow2, const TraceRhoParams &p, double K, int ctas, int threads,
+                                 cudaStream_t st) {
+    const size_t smem = trace_rho_smem_bytes(p, threads);
+#define NUFI_SW(DD, PP)                                                                               \
+    if (d == DD && ppt == PP) {                                                                       \
+        if (p.N == 16) return launch_one<DD, PP, true, 16, true>(p, K, ctas, threads, smem, st);      \
+        if (p.N == 32) return launch_one<DD, PP, true, 32, true>(p, K, ctas, threads, smem, st);      \
+        return pow2 ? launch_one<DD, PP, true, 0, true>(p, K, ctas, threads, smem, st)                \
+                    : launch_one<DD, PP, false, 0, true>(p, K, ctas, threads, smem, st);              \
+    }
+    NUFI_SW(1, 1)
+    NUFI_SW(2, 1)
+    NUFI_SW(3, 1)
+#undef NUFI_SW
+    return cudaErrorInvalidValue;
+}
+
+// per-CTA moment rows -> out[mom_count(d)] in a fixed order (one CTA)
+__global__ void reduce_moments_kernel(const double *__restrict__ part, int rows, int nm, int nsums, double measure,
+                                      double *__restrict__ out) {
+    __shared__ double sh[32];
+    for (int q = 0; q < nm; ++q) {
+        const bool is_sum = q < nsums, is_min = q == nsums;
+        double s = is_sum ? 0.0 : (is_min ? DBL_MAX : -DBL_MAX);
+        for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+            const double x = part[(size_t)r * nm + q];
+            s = is_sum ? s + x : (is_min ? fmin(s, x) : fmax(s, x));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double y = __shfl_xor_sync(0xffffffffu, s, o);
+            s = is_sum ? s + y : (is_min ? fmin(s, y) : fmax(s, y));
+        }
+        if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = sh[0];
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+                t = is_sum ? t + sh[w] : (is_min ? fmin(t, sh[w]) : fmax(t, sh[w]));
+            out[q] = is_sum ? t * measure : t;
+        }
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_reduce_moments(const double *part, int rows, int d, double measure, double *out, cudaStream_t st) {
+    reduce_moments_kernel<<<1, 256, 0, st>>>(part, rows, mom_sums(d) + 2, mom_sums(d), measure, out);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_reduce_blocks(const double *partial, const double *fminmax, double *out, int nodes,

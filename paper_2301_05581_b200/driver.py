@@ -85,14 +85,29 @@ class Simulation:
     """NuFI run state: device history + initial condition + tau, stepping to n_steps."""
 
     def __init__(self, grid: GridSpec, ic: InitialCondition, tau: float, n_steps: int, device: int | None = None,
-                 v_blocks: int = 0, stream: int | None = None):
+                 v_blocks: int = 0, stream: int | None = None, dtype=np.float64):
         if n_steps < 0:
             raise UsageError("n_steps must be >= 0")
         self.grid = grid
         self.n_steps = int(n_steps)
-        self.history = PotentialHistory(grid, tau, capacity=n_steps + 1, device=device, v_blocks=v_blocks,
-                                        stream=stream)
+        self.history = PotentialHistory(grid, tau, dtype=dtype, capacity=n_steps + 1, device=device,
+                                        v_blocks=v_blocks, stream=stream)
         self.ctx = FlowContext(history=self.history, ic=ic, tau=tau, grid=grid)
+
+    @classmethod
+    def resume(cls, path, grid: GridSpec, ic: InitialCondition, n_steps: int, device: int | None = None,
+               v_blocks: int = 0, stream: int | None = None) -> "Simulation":
+        """Continue a run from a VPHIST01 checkpoint (PotentialHistory.save, spline.py:157-194):
+        the history is the entire NuFI state (Eq. 26), so step len(history) is next."""
+        from .spline import read_checkpoint
+
+        grid_ck, dtype, tau, rows = read_checkpoint(path, grid)
+        if rows.shape[0] > n_steps + 1:
+            raise UsageError(f"checkpoint holds {rows.shape[0]} fields, more than n_steps + 1 = {n_steps + 1}")
+        sim = cls(grid, ic, tau, n_steps, device=device, v_blocks=v_blocks, stream=stream, dtype=dtype)
+        if rows.shape[0]:
+            sim.history.load_stack(rows.astype(np.float64).reshape((rows.shape[0],) + grid.shape_x))
+        return sim
 
     @property
     def n(self) -> int:

@@ -11,6 +11,7 @@ csrc/trace_common.cuh); `stacked()` / `entry()` copy rows back to the host.
 from __future__ import annotations
 
 import ctypes
+import struct
 from dataclasses import dataclass
 
 import numpy as np
@@ -57,23 +58,26 @@ class PotentialHistory:
     """Append-only sequence of spline fields on the GPU (spline.py:108-155).
 
     capacity: slabs preallocated (grown by doubling on demand, like
-    spline.py:136-139).  dtype: float64 only (the FP32 history mode of
-    spline.py:118-125 is not implemented).
+    spline.py:136-139).  dtype: float64, or float32 -- the reference's FP32
+    history mode (spline.py:118-125): every stored coefficient is rounded to
+    float32 on append and read back as double by the trace
+    (NUFI_FLAG_F32_HISTORY).
     """
 
     def __init__(self, grid: GridSpec, tau: float, dtype=np.float64, capacity: int = 16, device: int | None = None,
                  v_blocks: int = 0, block_range: tuple | None = None, stream: int | None = None):
         if tau <= 0:
             raise UsageError(f"time step must be positive, got {tau}")
-        if np.dtype(dtype) != np.dtype(np.float64):
-            raise UsageError("only float64 histories are supported on the GPU path")
+        self.dtype = np.dtype(dtype)
+        if self.dtype not in (np.dtype(np.float32), np.dtype(np.float64)):
+            raise UsageError(f"history dtype must be float32 or float64, got {self.dtype}")  # spline.py:123-125
         self.grid = grid
         self.tau = float(tau)
-        self.dtype = np.dtype(np.float64)
         self.device = _current_device() if device is None else int(device)
         lo, hi = block_range if block_range is not None else (0, 0)
+        self._flags = _lib.NUFI_FLAG_F32_HISTORY if self.dtype == np.float32 else 0
         cfg = _lib.make_config(grid, _placeholder_ic(grid), self.tau, max(1, int(capacity)) - 1, rho_bar=1.0,
-                               v_blocks=v_blocks, block_lo=lo, block_hi=hi)
+                               v_blocks=v_blocks, block_lo=lo, block_hi=hi, flags=self._flags)
         self._handle = _lib.Handle(cfg, self.device, stream)
         self.ic = None
 
@@ -87,7 +91,7 @@ class PotentialHistory:
         """Install f0 (and compute rho_bar on the device); returns rho_bar."""
         if ic.d != self.grid.d:
             raise UsageError(f"grid dimension {self.grid.d} does not match benchmark dimension {ic.d}")
-        cfg = _lib.make_config(self.grid, ic, self.tau, self.capacity - 1, rho_bar=rho_bar)
+        cfg = _lib.make_config(self.grid, ic, self.tau, self.capacity - 1, rho_bar=rho_bar, flags=self._flags)
         self._handle.call("nufi_set_initial_condition", ctypes.byref(cfg))
         self.ic = ic
         return self.rho_bar
@@ -132,7 +136,7 @@ class PotentialHistory:
             raise UsageError(f"history has {n} entries, requested {m}")
         out = np.empty(self.grid.n_nodes)
         self._handle.call("nufi_get_history", out.ctypes.data, int(m), 1)
-        out = out.reshape(self.grid.shape_x)
+        out = out.reshape(self.grid.shape_x).astype(self.dtype, copy=False)
         out.flags.writeable = False
         return SplineField(grid=self.grid, coeffs=out)
 
@@ -142,7 +146,7 @@ class PotentialHistory:
         out = np.empty((n, self.grid.n_nodes))
         if n:
             self._handle.call("nufi_get_history", out.ctypes.data, 0, n)
-        out = out.reshape((n,) + self.grid.shape_x)
+        out = out.reshape((n,) + self.grid.shape_x).astype(self.dtype, copy=False)
         out.flags.writeable = False
         return out
 
@@ -155,3 +159,55 @@ class PotentialHistory:
 
     def truncate(self, count: int) -> None:
         self._handle.call("nufi_truncate_history", int(count))
+
+    # -- checkpoint: the reference's VPHIST01 format (spline.py:105, 157-194) --
+
+    def save(self, path) -> None:
+        """Write the device history as VPHIST01: little-endian header <8sBBIQdd
+        (magic, d, itemsize, Nx, count, L, tau) + raw coefficient rows."""
+        with open(path, "wb") as fh:
+            fh.write(checkpoint_bytes(self.grid, self.dtype, self.tau, self.stacked()))
+
+    @classmethod
+    def load(cls, path, grid: GridSpec | None = None, capacity: int | None = None, device: int | None = None
+             ) -> "PotentialHistory":
+        """Reload a VPHIST01 file into a device history (spline.py:171-194); grid, when
+        given, supplies Nv and vmax and must match d, Nx, L."""
+        grid, dtype, tau, rows = read_checkpoint(path, grid)
+        count = rows.shape[0]
+        hist = cls(grid, tau, dtype=dtype, capacity=max(count, capacity or 0, 1), device=device)
+        if count:
+            hist.load_stack(rows.astype(np.float64).reshape((count,) + grid.shape_x))
+        return hist
+
+
+_MAGIC = b"VPHIST01"
+_HEADER = "<8sBBIQdd"
+
+
+def checkpoint_bytes(grid: GridSpec, dtype, tau: float, rows: np.ndarray) -> bytes:
+    """VPHIST01 image of `rows` (count, Nx, ..): header + little-endian rows (spline.py:157-169)."""
+    dtype = np.dtype(dtype)
+    rows = np.asarray(rows).reshape(-1, grid.n_nodes) if np.size(rows) else np.zeros((0, grid.n_nodes))
+    header = struct.pack(_HEADER, _MAGIC, grid.d, dtype.itemsize, grid.Nx, rows.shape[0], grid.L, float(tau))
+    return header + rows.astype(dtype.newbyteorder("<"), copy=False).tobytes()
+
+
+def read_checkpoint(path, grid: GridSpec | None = None):
+    """Parse a VPHIST01 file (spline.py:171-194) -> (grid, dtype, tau, rows (count, Nx^d))."""
+    with open(path, "rb") as fh:
+        head = fh.read(struct.calcsize(_HEADER))
+        if len(head) != struct.calcsize(_HEADER):
+            raise UsageError(f"{path} is not a potential-history file")
+        magic, d, itemsize, Nx, count, L, tau = struct.unpack(_HEADER, head)
+        if magic != _MAGIC:
+            raise UsageError(f"{path} is not a potential-history file")
+        dtype = np.dtype("<f4") if itemsize == 4 else np.dtype("<f8")
+        payload = np.frombuffer(fh.read(), dtype=dtype)
+    if grid is None:
+        grid = GridSpec(d=d, L=L, Nx=Nx, Nv=2, vmax=1.0)  # velocity grid unknown
+    elif (grid.d, grid.Nx) != (d, Nx) or abs(grid.L - L) > 1e-12 * L:
+        raise UsageError("checkpoint grid does not match the supplied grid")
+    if payload.size != count * Nx ** d:
+        raise UsageError(f"truncated history file: {path}")
+    return grid, np.dtype(f"=f{itemsize}"), float(tau), payload.reshape(count, Nx ** d)

@@ -52,6 +52,11 @@ CONFIGS = {
     "tiny2": dict(d=2, Nx=8, Nv=8, vmax=6.0, tau=1 / 8, N=24, bench="strong_landau_2d", alpha=0.5, keep=25),
     "tiny3": dict(d=3, Nx=8, Nv=4, vmax=6.0, tau=1 / 8, N=12, bench="two_stream_3d", alpha=None, keep=13),
     "eq1": dict(d=1, Nx=32, Nv=128, vmax=10.0, tau=1 / 16, N=160, bench="weak_landau_1d", alpha=0.0, keep=1),
+    # FP32 history mode (PotentialHistory(dtype=float32), spline.py:118-125)
+    "kat_wl_f32": dict(d=1, Nx=32, Nv=128, vmax=10.0, tau=1 / 16, N=160, bench="weak_landau_1d", alpha=None,
+                       keep=161, dtype="float32"),
+    "tiny2_f32": dict(d=2, Nx=8, Nv=8, vmax=6.0, tau=1 / 8, N=24, bench="strong_landau_2d", alpha=0.5, keep=25,
+                      dtype="float32"),
 }
 
 
@@ -97,7 +102,7 @@ def run(name, cfg):
     tau = cfg["tau"]
     N = cfg["N"]
     keep = cfg["keep"]
-    hist = spline.PotentialHistory(g, tau)
+    hist = spline.PotentialHistory(g, tau, dtype=np.dtype(cfg.get("dtype", "float64")))
     ctx = FlowContext(history=hist, ic=ic, tau=tau, grid=g)
     Xn = x_node_matrix(g)
     nodes = g.n_nodes
@@ -125,7 +130,7 @@ def run(name, cfg):
         evals.append(ctx.field_evals)
         if n < keep:
             rho[n] = r.density.values.reshape(-1)
-            coeffs[n] = np.asarray(fit.coeffs).reshape(-1)
+            coeffs[n] = np.asarray(hist.entry(n).coeffs, dtype=np.float64).reshape(-1)  # the stored slab
             E[n] = kernels.eval_E_many(fit.coeffs, g.L, Xn)
         if n % 50 == 0:
             print(f"[{name}] step {n}/{N}  W={W[n]:.6e}  t={time.time() - t0:.1f}s", flush=True)
@@ -172,6 +177,64 @@ def trace_goldens(name, g, stack, tau, n, M=2000, seed=1234):
     np.savez_compressed(os.path.join(OUT, f"trace_{name}.npz"), L=np.array(g.L), tau=np.array(tau), **out)
 
 
+# steps at which the observable sweep goldens are taken (Psi needs fields 0..n)
+SWEEP_N = {"kat_wl": (0, 1, 20, 40), "tiny2": (0, 3, 10, 20), "tiny3": (0, 2, 6, 11), "wl3r": (0, 5, 16)}
+
+
+def conserved_weights():
+    """The conserved-quantity weights of SPEC.md:403-406 as quadrature_sweep weights
+    (f, f^2, f ln f with 0 ln 0 := 0, |v|^2 f / 2, v f)."""
+
+    def f_ln_f(X, V, F):
+        safe = np.where(F > 0, F, 1.0)
+        return np.where(F > 0, F * np.log(safe), 0.0)
+
+    return [
+        lambda X, V, F: F,
+        lambda X, V, F: F * F,
+        f_ln_f,
+        lambda X, V, F: 0.5 * np.sum(V * V, axis=1) * F,
+        lambda X, V, F: V * F[:, None],
+    ]
+
+
+def sweep_goldens(name, g, ic, stack, tau):
+    """density.quadrature_sweep_many (density.py:104-120, numba backend) with the
+    conserved-quantity weights at the steps SWEEP_N[name], through a stored history."""
+    from vpflow import density, spline
+    from vpflow.flow import FlowContext
+
+    hist = spline.PotentialHistory(g, tau)
+    for c in stack:
+        hist.append(spline.SplineField(grid=g, coeffs=np.ascontiguousarray(c)))
+    ctx = FlowContext(history=hist, ic=ic, tau=tau, grid=g)
+    steps = [n for n in SWEEP_N[name] if n + 1 <= len(stack)]
+    rows = []
+    evals = []
+    for n in steps:
+        ctx.field_evals = 0
+        f, f2, flnf, kin, mom = density.quadrature_sweep_many(ctx, n, conserved_weights())
+        rows.append([f, f2, flnf, kin] + list(np.atleast_1d(mom)))
+        evals.append(ctx.field_evals)
+    np.savez_compressed(os.path.join(OUT, f"sweep_{name}.npz"), steps=np.array(steps), moments=np.array(rows),
+                        field_evals=np.array(evals, dtype=np.int64),
+                        columns=np.array(["f", "f2", "f_ln_f", "kinetic"] + [f"mom{a}" for a in range(g.d)]))
+
+
+def checkpoint_goldens():
+    """VPHIST01 files written by the reference's PotentialHistory.save (spline.py:157-169)."""
+    from vpflow import spline
+
+    for base, rows, dtype in (("kat_wl", 20, "float64"), ("tiny2_f32", 10, "float32")):
+        g, _ = build(CONFIGS[base])
+        z = np.load(os.path.join(OUT, f"{base}.npz"))
+        stack = z["coeffs"].reshape((-1,) + (g.Nx,) * g.d)[:rows]
+        hist = spline.PotentialHistory(g, CONFIGS[base]["tau"], dtype=np.dtype(dtype))
+        for c in stack:
+            hist.append(spline.SplineField(grid=g, coeffs=np.ascontiguousarray(c)))
+        hist.save(os.path.join(OUT, f"{base}_{rows}.vphist"))
+
+
 def host_info():
     try:
         cpu = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
@@ -187,6 +250,16 @@ def main(argv):
     sys.path.insert(0, REF)
     names = argv or list(CONFIGS)
     for name in names:
+        if name == "checkpoints":
+            checkpoint_goldens()
+            continue
+        if name.startswith("sweep_"):
+            base = name[len("sweep_"):]
+            g, ic = build(CONFIGS[base])
+            z = np.load(os.path.join(OUT, f"{base}.npz"))
+            stack = z["coeffs"].reshape((-1,) + (g.Nx,) * g.d)
+            sweep_goldens(base, g, ic, stack, CONFIGS[base]["tau"])
+            continue
         if name.startswith("trace_"):
             # trace goldens only, from the coefficients stored by an earlier run
             base = name[len("trace_"):]

@@ -16,7 +16,7 @@ from oracle import oracle as O
 from tests._util import golden, normwise
 
 TRACE_CASES = ["kat_wl", "tiny2", "tiny3", "wl3r"]
-LOOP_CASES = ["kat_wl", "eq1", "tiny2", "tiny3", "wl1"]
+LOOP_CASES = ["kat_wl", "eq1", "tiny2", "tiny3", "wl1", "kat_wl_f32", "tiny2_f32"]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -65,7 +65,7 @@ def test_loop_vs_reference(name):
         pytest.skip("golden not generated")
     N = len(g["W"]) - 1
     keep = g["rho"].shape[0]
-    run = O.OracleRun(O.case(name)).run(N, keep)
+    run = O.OracleRun(O.case(name), f32=name.endswith("_f32")).run(N, keep)
     assert normwise(run["rho"], g["rho"]).max() <= 1e-12
     assert normwise(run["coeffs"], g["coeffs"]).max() <= 1e-12
     assert normwise(run["E"], g["E"]).max() <= 1e-12
@@ -115,3 +115,23 @@ def test_kat_poisson_eigenfunction():
 def test_kat_equilibrium():
     """alpha = 0: W < 1e-20 at every step."""
     assert np.all(golden("eq1")["W"] < 1e-20)
+
+
+@pytest.mark.parametrize("name", ["kat_wl", "tiny2", "tiny3", "wl3r"])
+def test_sweep_vs_reference(name):
+    """Oracle quadrature_sweep_many (Psi) vs the reference's, conserved-quantity weights."""
+    z = golden(f"sweep_{name}")
+    base = golden(name)
+    if z is None or base is None:
+        pytest.skip("sweep golden missing")
+    c = O.case(name)
+    run = O.OracleRun(c)
+    stack = base["coeffs"]
+    for i, n in enumerate(z["steps"]):
+        run.field_evals = 0
+        f, f2, flnf, kin, mom = run.quadrature_sweep_many(int(n), O.conserved_weights(), stack=stack)
+        got = np.array([f, f2, flnf, kin] + list(np.atleast_1d(mom)))
+        ref = z["moments"][i]
+        scale = np.abs(ref[:4]).max()
+        assert np.abs(got - ref).max() <= 1e-12 * scale, (n, got - ref)
+        assert run.field_evals == int(z["field_evals"][i])
