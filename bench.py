@@ -263,9 +263,15 @@ def gpu_arm(args, rank: int, world: int):
     peak_ms = ctypes.c_double()
     lib.nufi_fp64_peak(dev, ctypes.byref(peak), ctypes.byref(peak_ms))
     achieved = ALGO_FLOPS[g.d] * trace_ps / (trace_ms * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(args.config)
     roofline = {
         "bound": "fp64", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
-        "frac": achieved / peak.value if peak.value else None, "traffic": None,
+        "frac": achieved / peak.value if peak.value else None,
+        "traffic": traffic["traffic"] if traffic else None,
+        "traffic_detail": traffic,
         "kernel": ("run_1d_kernel (persistent: all steps, trace + grid barrier + field tail)" if g.d == 1
                    else f"trace_rho_kernel<{g.d}>"), "algo_flops_per_point_step": ALGO_FLOPS[g.d],
         "trace_launches": int(trace_launches), "trace_ms_per_launch": trace_ms / max(1, trace_launches),

@@ -34,15 +34,6 @@ cudaError_t launch_trace_rho_1d(const TraceRhoParams &p, const FieldParams &fp, 
 int trace_rho_1d_sps(int N);
 cudaError_t launch_field_tables(double *tw, double *fac, double *k2, int d, int N, int nodes, double k_scale,
                                 cudaStream_t st);
-struct Run1DParams {
-    TraceRhoParams tp;
-    FieldParams fp;
-    int n_first, n_last;
-    double *rho_hist, *E_hist, *W_hist, *stats_hist;
-    unsigned *barrier;
-    int tiles;
-    unsigned long long *stamps;
-};
 cudaError_t launch_run_1d(const Run1DParams &P, int threads, int device, cudaStream_t st, int *grid_out);
 cudaError_t launch_build_ev_slabs(double *hist, double *ev_hist, int d, int N, int nodes, int ev_slab_elems,
                                   double K, int64_t r0, int64_t r1, int f32, cudaStream_t st);
@@ -423,8 +414,9 @@ int nufi_create(const nufi_config *cfg, int device, void *stream, nufi_handle **
     const size_t nodes = h->nodes;
     CU(cudaMalloc(&h->hist, h->cap * nodes * sizeof(double)));
     CU(cudaMalloc(&h->ev_hist, h->cap * (size_t)h->ev_elems * sizeof(double)));
-    CU(cudaMalloc(&h->partial, (size_t)h->vt_total * nodes * sizeof(double)));
-    CU(cudaMalloc(&h->fminmax, (size_t)h->vt_total * h->node_tiles * 2 * sizeof(double)));
+    // x2: the persistent d = 1 run kernel double-buffers the tile partials by step parity
+    CU(cudaMalloc(&h->partial, 2 * (size_t)h->vt_total * h->node_tiles * 32 * sizeof(double)));
+    CU(cudaMalloc(&h->fminmax, 2 * (size_t)h->vt_total * h->node_tiles * 2 * sizeof(double)));
     CU(cudaMalloc(&h->blocks, ((size_t)h->B * nodes + 2 * h->B) * sizeof(double)));
     CU(cudaMalloc(&h->d_rho, nodes * sizeof(double)));
     CU(cudaMalloc(&h->d_E, nodes * c.d * sizeof(double)));
@@ -548,6 +540,8 @@ static TraceRhoParams trace_params(nufi_handle *h, int64_t n, int b_lo) {
     p.vt_rows = h->vt_rows;
     p.passes = h->passes;
     p.vt_lo = b_lo * h->vt_per_block;
+    p.B = h->B;
+    p.vt_per_block = h->vt_per_block;
     p.n = (int)n;
     p.hx = h->hx;
     p.inv_h = h->inv_h;
@@ -861,6 +855,10 @@ int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, d
         P.stats_hist = base_dev[3];
         P.barrier = h->barrier;
         P.tiles = h->B * h->vt_per_block * h->node_tiles;
+        P.blocks = h->blocks;
+        // two-level combine when every CTA re-reading all tile partials would dominate the tail
+        P.two_level = (int64_t)h->vt_total * h->nodes > 16384 ? 1 : 0;
+        if (const char *e = getenv("NUFI_TWO_LEVEL")) P.two_level = atoi(e);
         static const char *stamp_path = getenv("NUFI_STAMPS");  // debug: per-step phase timestamps
         unsigned long long *stamps = nullptr;
         if (stamp_path) CU(cudaMalloc(&stamps, (3 * steps + 10 + 6 * 1024) * sizeof(unsigned long long)));

@@ -60,6 +60,19 @@ struct FieldParams {
     unsigned long long *tstamps;  // debug: phase timestamps (thread 0), 10 slots
 };
 
+// d = 1 whole-run persistent kernel (run_1d.cu)
+struct Run1DParams {
+    TraceRhoParams tp;  // geometry / arithmetic (tp.n unused)
+    FieldParams fp;     // tail template (slot and outputs set per step)
+    int n_first, n_last;
+    double *rho_hist, *E_hist, *W_hist, *stats_hist;  // device rows (n - n_first), nullable
+    unsigned *barrier;                                // zero at launch
+    int tiles;                                        // node_tiles * v-tiles
+    unsigned long long *stamps;                       // optional: CTA 0 globaltimer per step x 3
+    double *blocks;   // two-level combine: B * nodes block sums + B (min, max)
+    int two_level;    // combine tile partials across the grid first (second grid barrier)
+};
+
 #define NUFI_STAMP(p, k)                                                              \
     do {                                                                              \
         if ((p).tstamps && threadIdx.x == 0) {                                        \
@@ -146,6 +159,88 @@ __device__ __forceinline__ void dft_pass(const double *__restrict__ ire, const d
         }
     }
     __syncthreads();
+}
+
+// c = gc (*) r and phi = gp (*) r for small N (power of two): one output per
+// group of G lanes, conflict-free kernel-tap loads (consecutive j across groups).
+static __device__ __forceinline__ void circulant_direct(const double *gc, const double *gp, const double *r, double *c,
+                                                        double *phi, int N) {
+    const int T = blockDim.x;
+    int G = 1;
+    while (G < 32 && 2 * G <= N && 2 * N * (2 * G) <= T) G *= 2;
+    const int part = threadIdx.x % G;
+    for (int base = 0; base < 2 * N; base += T / G) {  // warp-uniform trip count
+        const int o = base + threadIdx.x / G;
+        const bool active = o < 2 * N;
+        const int j = !active ? 0 : (o < N ? o : o - N);
+        const double *g = o < N ? gc : gp;
+        double a0 = 0.0, a1 = 0.0;
+        int i = part;
+        for (; i + G < N; i += 2 * G) {
+            a0 = fma(g[(j - i + N) & (N - 1)], r[i], a0);
+            a1 = fma(g[(j - i - G + N) & (N - 1)], r[i + G], a1);
+        }
+        if (i < N) a0 = fma(g[(j - i + N) & (N - 1)], r[i], a0);
+        double a = a0 + a1;
+        for (int q = G >> 1; q > 0; q >>= 1) a += __shfl_xor_sync(0xffffffffu, a, q, G);
+        if (active && part == 0) (o < N ? c : phi)[j] = a;
+    }
+}
+
+// In-place radix-2 complex FFT of length N = 2^logN on shared arrays (re, im) whose
+// input is already in bit-reversed order; sign -1: forward e^{-2 pi i jk/N}, +1:
+// unscaled inverse.  twc / tws: cos / sin(2 pi m / N), m < N.  One butterfly per
+// thread per stage, a CTA barrier between stages.
+static __device__ __forceinline__ void fft_radix2(double *re, double *im, const double *twc, const double *tws, int N,
+                                                  double sign) {
+    for (int half = 1; half < N; half <<= 1) {
+        const int stride = N / (2 * half);
+        for (int b = threadIdx.x; b < N / 2; b += blockDim.x) {
+            const int pos = b & (half - 1);
+            const int i0 = ((b - pos) << 1) + pos, i1 = i0 + half;
+            const double wr = twc[pos * stride], wi = sign * tws[pos * stride];
+            const double ur = re[i1], ui = im[i1];
+            const double xr = fma(ur, wr, -ui * wi), xi = fma(ur, wi, ui * wr);
+            const double ar = re[i0], ai = im[i0];
+            re[i1] = ar - xr;
+            im[i1] = ai - xi;
+            re[i0] = ar + xr;
+            im[i0] = ai + xi;
+        }
+        __syncthreads();
+    }
+}
+
+// c + i phi = IFFT_unscaled( FFT(r) * fac * (1 + i sym) ): the d = 1 Poisson solve +
+// spline fit in O(N log N) (fac = 1 / (N k^2 sym), 0 at the zero / Nyquist modes;
+// poisson.py:105-110, spline.py:78-84).  Both products are real-even factors on a
+// Hermitian spectrum, so c and phi come out as the real and imaginary parts of ONE
+// inverse transform.  tw: 2N shared doubles for the twiddles.
+static __device__ __forceinline__ void circulant_fft(const FieldParams &p, const double *r, double *c, double *phi,
+                                                     double *twc, double *tws, int N) {
+    const int logN = 31 - __clz(N);
+    for (int m = threadIdx.x; m < N; m += blockDim.x) {
+        twc[m] = p.twc[m];
+        tws[m] = p.tws[m];
+        const int br = (int)(__brev((unsigned)m) >> (32 - logN));
+        c[br] = r[m];
+        phi[br] = 0.0;
+    }
+    __syncthreads();
+    fft_radix2(c, phi, twc, tws, N, -1.0);
+    for (int k = threadIdx.x; k < N; k += blockDim.x) {
+        const int kb = (int)(__brev((unsigned)k) >> (32 - logN));
+        if (k <= kb) {  // multiply and bit-reverse in place (disjoint swap pairs)
+            const double f0 = p.fac[k], s0 = p.fac[N + k], f1 = p.fac[kb], s1 = p.fac[N + kb];
+            const double a0 = c[k] * f0, b0 = phi[k] * f0, a1 = c[kb] * f1, b1 = phi[kb] * f1;
+            c[kb] = fma(-b0, s0, a0);
+            phi[kb] = fma(a0, s0, b0);
+            c[k] = fma(-b1, s1, a1);
+            phi[k] = fma(a1, s1, b1);
+        }
+    }
+    __syncthreads();
+    fft_radix2(c, phi, twc, tws, N, 1.0);
 }
 
 // d = 1 tail: the Poisson solve + spline fit is a circulant operator on the
@@ -242,29 +337,11 @@ static __device__ __forceinline__ bool field_update_1d_body(const FieldParams &p
     if (p.finish_only) return true;
     __syncthreads();
     NUFI_STAMP(p, 2);
-    // ---- c = gc (*) rho', phi = gp (*) rho': 2N outputs, G lanes each ----
-    {
-        int G = 1;
-        while (G < 32 && 2 * G <= N && 2 * N * (2 * G) <= T) G *= 2;
-        const int part = threadIdx.x % G;
-        for (int o = threadIdx.x / G; o < 2 * N; o += T / G) {
-            const int j = o < N ? o : o - N;
-            const double *g = o < N ? gc : gp;
-            double a0 = 0.0, a1 = 0.0;
-            int i = part;
-            for (; i + G < N; i += 2 * G) {
-                a0 = fma(g[(j - i + N) & (N - 1)], r[i], a0);
-                a1 = fma(g[(j - i - G + N) & (N - 1)], r[i + G], a1);
-            }
-            if (i < N) a0 = fma(g[(j - i + N) & (N - 1)], r[i], a0);
-            double a = a0 + a1;
-            if (G > 1) {
-                const unsigned mask = __activemask();
-                for (int q = G >> 1; q > 0; q >>= 1) a += __shfl_xor_sync(mask, a, q, G);
-            }
-            if (part == 0) (o < N ? c : phi)[j] = a;
-        }
-    }
+    // ---- c = gc (*) rho', phi = gp (*) rho': 2N outputs ----
+    if (N >= 128)
+        circulant_fft(p, r, c, phi, gc, gp, N);  // gc / gp smem reused for the twiddles
+    else
+        circulant_direct(gc, gp, r, c, phi, N);
     __syncthreads();
     NUFI_STAMP(p, 4);
     // ---- W (Parseval) and the neutrality check (poisson.py:97-104) in warp 0 ----

@@ -171,6 +171,8 @@ struct TraceRhoParams {
     int vt_rows;    // v-rows per CTA tile (warps * PPT * passes)
     int passes;
     int vt_lo;      // first global v-tile traced by this launch
+    int B;          // velocity blocks (fixed combine order; the multi-rank shard unit)
+    int vt_per_block;
     // step
     int n;          // Psi-tilde through slabs n-1 .. 0
     // arithmetic (scaled units: X = x*inv_h - 1/2, V = v*tau*inv_h)

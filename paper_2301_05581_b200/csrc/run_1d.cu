@@ -25,15 +25,6 @@
 
 namespace nufi {
 
-struct Run1DParams {
-    TraceRhoParams tp;  // geometry / arithmetic (tp.n unused)
-    FieldParams fp;     // tail template (slot and outputs set per step)
-    int n_first, n_last;
-    double *rho_hist, *E_hist, *W_hist, *stats_hist;  // device rows (n - n_first), nullable
-    unsigned *barrier;                                // zero at launch
-    int tiles;                                        // node_tiles * v-tiles
-    unsigned long long *stamps;                       // optional: CTA 0 globaltimer per step x 3
-};
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -111,6 +102,10 @@ __global__ void __launch_bounds__(288, 2) run_1d_kernel(const Run1DParams P) {
     for (int n = P.n_first; n <= P.n_last; ++n) {
         const int m = n >= 1 ? n - 1 : 0;  // slabs streamed by TMA: m-1 .. 0
         const int groups = (m + SPS - 1) / SPS;
+        // partials double-buffered by step parity: a CTA that finished the tail of
+        // step n may write step n+1's partials while a slower one still reads step n's
+        double *part = p.partial + (size_t)(n & 1) * P.tiles * 32;
+        double *fmm = p.fminmax + (size_t)(n & 1) * P.tiles * 2;
         const int top_cnt = m - (groups - 1) * SPS;
 
         for (int tile = blockIdx.x; tile < P.tiles; tile += gridDim.x) {
@@ -141,7 +136,7 @@ __global__ void __launch_bounds__(288, 2) run_1d_kernel(const Run1DParams P) {
                 }
             } else {
                 const bool valid = node < nodes;
-                const int j = vt * p.vt_rows + warp;
+                const int j = d1_row(vt, warp, p.vt_per_block, p.B);
                 const double v0 = __dadd_rn(-p.vmax, __dmul_rn((double)j + 0.5, p.hv));  // grids.py:110-115
                 double V = v0 * p.vel_to_scaled;
                 double X = ((double)(valid ? node : 0) - 0.5) - V;  // first drift (folded form)
@@ -201,7 +196,7 @@ __global__ void __launch_bounds__(288, 2) run_1d_kernel(const Run1DParams P) {
                     mn = fmin(mn, red[32 * cw + w * 32 + lane]);
                     mx = fmax(mx, red[64 * cw + w * 32 + lane]);
                 }
-                if (node < nodes) p.partial[(size_t)vt * nodes + node] = sum;
+                if (node < nodes) part[(size_t)vt * nodes + node] = sum;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
                     mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
@@ -209,8 +204,8 @@ __global__ void __launch_bounds__(288, 2) run_1d_kernel(const Run1DParams P) {
                 }
                 if (lane == 0) {
                     const size_t c = (size_t)vt * p.node_tiles + nt;
-                    p.fminmax[2 * c] = mn;
-                    p.fminmax[2 * c + 1] = mx;
+                    fmm[2 * c] = mn;
+                    fmm[2 * c + 1] = mx;
                 }
             }
             __syncthreads();
@@ -227,8 +222,64 @@ __global__ void __launch_bounds__(288, 2) run_1d_kernel(const Run1DParams P) {
         grid_barrier(P.barrier, ++gen * gridDim.x);
         if (P.stamps && blockIdx.x == 0 && threadIdx.x == 0) P.stamps[3 * (n - P.n_first) + 1] = globaltimer();
 
-        // redundant tail in every CTA; CTA 0 publishes
         FieldParams fp = P.fp;
+        fp.sums = part;
+        fp.minmax = fmm;
+        if (P.two_level) {
+            // level 1, spread over the grid: tile partials -> block sums in the SAME
+            // sequential order the tail uses (field_update_1d_body), block (min, max)
+            const int B = fp.B, rpb = fp.rows_per_block;
+            const int64_t outs = (int64_t)B * nodes;
+            for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < outs;
+                 o += (int64_t)gridDim.x * blockDim.x) {
+                const int b = (int)(o / nodes), i = (int)(o - (int64_t)b * nodes);
+                const double *src = fp.sums + (size_t)b * rpb * nodes + i;
+                double Sb = 0.0;
+                int q = 0;
+                for (; q + 8 <= rpb; q += 8) {
+                    double v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (size_t)(q + u) * nodes);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) Sb += v[u];
+                }
+                for (; q < rpb; ++q) Sb += __ldcg(src + (size_t)q * nodes);
+                P.blocks[o] = Sb;
+            }
+            for (int b = blockIdx.x; b < B; b += gridDim.x) {
+                double mn = DBL_MAX, mx = -DBL_MAX;
+                for (int q = threadIdx.x; q < fp.mm_per_block; q += blockDim.x) {
+                    mn = fmin(mn, __ldcg(fp.minmax + 2 * ((size_t)b * fp.mm_per_block + q)));
+                    mx = fmax(mx, __ldcg(fp.minmax + 2 * ((size_t)b * fp.mm_per_block + q) + 1));
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                }
+                if (lane == 0) {
+                    red[warp] = mn;
+                    red[32 + warp] = mx;
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+                        mn = fmin(mn, red[w]);
+                        mx = fmax(mx, red[32 + w]);
+                    }
+                    P.blocks[outs + 2 * b] = mn;
+                    P.blocks[outs + 2 * b + 1] = mx;
+                }
+                __syncthreads();
+            }
+            grid_barrier(P.barrier, ++gen * gridDim.x);
+            fp.sums = P.blocks;
+            fp.rows_per_block = 1;
+            fp.minmax = P.blocks + outs;
+            fp.mm_per_block = 1;
+        }
+
+        // redundant tail in every CTA; CTA 0 publishes
         fp.slot = n;
         fp.ev_local = slabN;
         const int64_t row = n - P.n_first;

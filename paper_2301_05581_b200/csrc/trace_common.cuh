@@ -44,6 +44,16 @@ __host__ __device__ inline int ev_halo_source(int d, int N, int e) {
     }
     return lin;
 }
+// d = 1 velocity row of warp slot w of global v-tile vt.  Block b is the residue
+// class {j : j mod B == b}; inside a block the tile's rows are strided across the
+// whole block (local row l = t + vt_per_block * w), so every CTA tile -- and every
+// rank's share of blocks -- mixes trapped (chaotic, bank-conflicted gathers) and
+// passing (coherent) particles: equal work per CTA between grid barriers.
+__host__ __device__ __forceinline__ int d1_row(int vt, int w, int vt_per_block, int B) {
+    const int b = vt / vt_per_block, t = vt - b * vt_per_block;
+    return (t + vt_per_block * w) * B + b;
+}
+
 // conserved-quantity sweep: sums f, f^2, f ln f, |v|^2 f / 2, v_a f (then f_min, f_max)
 __host__ __device__ constexpr int mom_sums(int d) { return 4 + d; }
 

@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(288) trace_rho_1d_kernel(const TraceRhoParams 
         }
     } else {
         // point (x_i, v_j): grids.py:104-115
-        const int j = vt * p.vt_rows + warp;
+        const int j = d1_row(vt, warp, p.vt_per_block, p.B);
         const double v0 = __dadd_rn(-p.vmax, __dmul_rn((double)j + 0.5, p.hv));
         double V = v0 * p.vel_to_scaled;
         double X = ((double)(valid ? node : 0) - 0.5) - V;  // first drift (folded form)
