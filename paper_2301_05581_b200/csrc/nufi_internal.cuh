@@ -78,19 +78,24 @@ __device__ __forceinline__ int locate_centred(double X, int N, double &fc) {
     return i < 0 ? i + N : i;
 }
 
-// Cubic B-spline stencil weights and their t-derivatives at fraction f
-// (kernels.py:62-81 / 211-221), FMA form.
-__device__ __forceinline__ void bspline_w_dw(double f, double w[4], double dw[4]) {
-    const double s = 1.0 - f;
+// Cubic B-spline stencil weights and their t-derivatives (kernels.py:62-81 /
+// 211-221), SCALED: w'' = 6 w, dw'' = 2 dw, from the centred fraction fc
+// (f = fc + 1/2), FMA form.  The scale factors are folded into the kick constant
+// (trace_common.cuh: K / 12 in d = 2, K / 72 in d = 3), which saves the four
+// constant multiplies per axis of the unscaled form:
+//   w0'' = s^3          w1'' = 4 - 6 f^2 + 3 f^3   w2'' = 4 - 6 s^2 + 3 s^3   w3'' = f^3
+//   dw0'' = -s^2        dw1'' = f (3 f - 4)        dw2'' = s (4 - 3 s)        dw3'' = f^2
+__device__ __forceinline__ void bspline_w_dw_scaled(double fc, double w[4], double dw[4]) {
+    const double f = fc + 0.5, s = 0.5 - fc;
     const double f2 = f * f, s2 = s * s;
-    w[0] = s2 * s * (1.0 / 6.0);
-    w[1] = fma(-f2, fma(-0.5, f, 1.0), 2.0 / 3.0);
-    w[2] = fma(-s2, fma(-0.5, s, 1.0), 2.0 / 3.0);
-    w[3] = f2 * f * (1.0 / 6.0);
-    dw[0] = -0.5 * s2;
-    dw[1] = f * fma(1.5, f, -2.0);
-    dw[2] = s * fma(-1.5, s, 2.0);
-    dw[3] = 0.5 * f2;
+    w[0] = s2 * s;
+    w[1] = fma(f2, fma(3.0, f, -6.0), 4.0);
+    w[2] = fma(s2, fma(3.0, s, -6.0), 4.0);
+    w[3] = f2 * f;
+    dw[0] = -s2;
+    dw[1] = f * fma(3.0, f, -4.0);
+    dw[2] = s * fma(-3.0, s, 4.0);
+    dw[3] = f2;
 }
 
 // ----------------------------------------------------------------------------

@@ -88,8 +88,8 @@ __device__ __forceinline__ void kick(const double (&X)[D], double (&V)[D], const
         const int ix = locate_centred<POW2>(X[0], N, fx);
         const int iy = locate_centred<POW2>(X[1], N, fy);
         double wx[4], dwx[4], wy[4], dwy[4];
-        bspline_w_dw(fx + 0.5, wx, dwx);
-        bspline_w_dw(fy + 0.5, wy, dwy);
+        bspline_w_dw_scaled(fx, wx, dwx);
+        bspline_w_dw_scaled(fy, wy, dwy);
         const double *c = slab + ix * R + iy;
         double gx = 0.0, gy = 0.0;
 #pragma unroll
@@ -101,7 +101,7 @@ __device__ __forceinline__ void kick(const double (&X)[D], double (&V)[D], const
             gx = fma(dwx[m], r, gx);
             gy = fma(wx[m], rd, gy);
         }
-        const double k = half ? 0.5 * K : K;
+        const double k = (half ? 0.5 : 1.0) * (K * (1.0 / 12.0));  // scaled weights: 2 * 6
         V[0] = fma(k, gx, V[0]);
         V[1] = fma(k, gy, V[1]);
     } else {
@@ -111,9 +111,9 @@ __device__ __forceinline__ void kick(const double (&X)[D], double (&V)[D], const
         const int iy = locate_centred<POW2>(X[1], N, fy);
         const int iz = locate_centred<POW2>(X[2], N, fz);
         double wx[4], dwx[4], wy[4], dwy[4], wz[4], dwz[4];
-        bspline_w_dw(fx + 0.5, wx, dwx);
-        bspline_w_dw(fy + 0.5, wy, dwy);
-        bspline_w_dw(fz + 0.5, wz, dwz);
+        bspline_w_dw_scaled(fx, wx, dwx);
+        bspline_w_dw_scaled(fy, wy, dwy);
+        bspline_w_dw_scaled(fz, wz, dwz);
         const double *c = slab + (ix * R + iy) * R + iz;
         double gx = 0.0, gy = 0.0, gz = 0.0;
 #pragma unroll
@@ -133,7 +133,7 @@ __device__ __forceinline__ void kick(const double (&X)[D], double (&V)[D], const
             gy = fma(wx[m], sdy, gy);
             gz = fma(wx[m], sdz, gz);
         }
-        const double k = half ? 0.5 * K : K;
+        const double k = (half ? 0.5 : 1.0) * (K * (1.0 / 72.0));  // scaled weights: 2 * 6 * 6
         V[0] = fma(k, gx, V[0]);
         V[1] = fma(k, gy, V[1]);
         V[2] = fma(k, gz, V[2]);

@@ -3,7 +3,9 @@
 One process per GPU (torch.distributed, NCCL over NVLink for the plumbing).
 The Nv^d velocity rows are cut into B fixed blocks (default 8, independent of
 the rank count); rank r traces blocks [r*B/G, (r+1)*B/G) for every x node
-(contiguous v-row sharding).  Each rank's
+(v-row sharding; d >= 2 blocks are contiguous row ranges,
+d = 1 blocks are residue classes j mod B so every rank -- and every CTA tile --
+mixes trapped and passing particles, csrc/trace_common.cuh d1_row).  Each rank's
 nufi_rho_partials writes its blocks' per-node v-sums into a
 (B*Nx^d + 2B)-double buffer and zeros elsewhere, so one SUM allreduce gives
 every rank the complete block table exactly (one non-zero contributor per

@@ -32,7 +32,10 @@ def block_table(c, run, n, blocks):
     X0 = O.x_node_matrix(c)
     V0 = O.v_mid_matrix(c)
     for b in blocks:
-        V = np.tile(V0[b * per:(b + 1) * per], (nodes, 1))
+        # d = 1: block b is the residue class {j : j mod B == b} (csrc/trace_common.cuh
+        # d1_row); d >= 2: contiguous rows
+        rows = np.arange(b, cells, B) if c.d == 1 else np.arange(b * per, (b + 1) * per)
+        V = np.tile(V0[rows], (nodes, 1))
         X = np.repeat(X0, per, axis=0)
         if n > 0:
             O.trace_backward(stack, c.L, n, c.tau, X, V, False)

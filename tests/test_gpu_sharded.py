@@ -1,0 +1,68 @@
+"""The multi-rank device path on one GPU, ranks emulated in one process.
+
+Each emulated rank owns a handle tracing its velocity blocks (nufi_rho_partials);
+the allreduce is emulated by summing the ranks' zero-padded block tables (exact:
+one non-zero contributor per element, x + 0 = x); every rank then runs the
+redundant combine + field update (nufi_step_finish).  The ranks' launches are
+independent and sequential (no kernel waits on another rank).  Required:
+per-step rho / W and the full coefficient history bit-identical across ranks and
+to the single-GPU run (the block combine order does not depend on the rank count).
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2301_05581_b200 as nufi
+from paper_2301_05581_b200.configs import workload
+from paper_2301_05581_b200.dist import block_range
+
+pytestmark = pytest.mark.gpu
+
+
+def sharded_run(name, N, world, B=8):
+    w = workload(name)
+    g = w.grid
+    ranks = []
+    for r in range(world):
+        h = nufi.PotentialHistory(g, w.tau, capacity=N + 1, v_blocks=B, block_range=block_range(B, r, world))
+        nufi.FlowContext(history=h, ic=w.ic, tau=w.tau, grid=g)  # binds f0
+        n_part = int(h.handle.lib.nufi_partials_len(h.handle.h))
+        ranks.append((h, torch.zeros(n_part, dtype=torch.float64, device="cuda")))
+    rho = np.empty((world, N + 1, g.n_nodes))
+    W = np.empty((world, N + 1))
+    evals = 0
+    for n in range(N + 1):
+        for h, part in ranks:
+            ev = ctypes.c_int64(0)
+            h.handle.call("nufi_rho_partials", n, part.data_ptr(), ctypes.byref(ev))
+            evals += ev.value
+        torch.cuda.synchronize()
+        table = sum(p for _, p in ranks)  # the allreduce
+        torch.cuda.synchronize()
+        for r, (h, _) in enumerate(ranks):
+            out_rho = np.empty(g.n_nodes)
+            out_W = np.empty(1)
+            h.handle.call("nufi_step_finish", n, table.data_ptr(), out_rho.ctypes.data, None, out_W.ctypes.data,
+                          None)
+            rho[r, n] = out_rho
+            W[r, n] = out_W[0]
+    hists = [h.stacked().reshape(N + 1, -1) for h, _ in ranks]
+    return rho, W, hists, evals
+
+
+@pytest.mark.parametrize("name,N", [("kat_wl", 40), ("tiny2", 12), ("tiny3", 8)])
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_bit_identical_to_single_gpu(name, N, world):
+    w = workload(name)
+    sim = nufi.Simulation(w.grid, w.ic, w.tau, N, v_blocks=8)
+    ref = sim.run()
+    rho, W, hists, evals = sharded_run(name, N, world)
+    ref_hist = sim.history.stacked().reshape(N + 1, -1)
+    for r in range(world):
+        assert np.array_equal(rho[r], ref.rho), (r, np.abs(rho[r] - ref.rho).max())
+        assert np.array_equal(W[r], ref.W)
+        assert np.array_equal(hists[r], ref_hist)
+    assert evals == ref.field_evals
