@@ -160,6 +160,27 @@ def reference_arm(args, rank: int):
 # GPU arm
 # ---------------------------------------------------------------------------
 
+def smem_roofline(torch, dev, d, trace_ps, trace_ms):
+    """The co-limiter of the gather stencil: algorithmic coefficient bytes (4^d doubles
+    per point-step) over the shared-memory crossbar, 128 B/clk/SM
+    (B300_MICROARCH.md LDS/STS table; no measured B200 figure exists) x SMs x max clock."""
+    from paper_2301_05581_b200.configs import ALGO_BYTES
+
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    mhz = 1965.0
+    try:
+        mhz = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"])
+    except Exception:
+        pass
+    peak = 128.0 * sms * mhz * 1e6 / 1e9
+    achieved = ALGO_BYTES[d] * trace_ps / (trace_ms * 1e-3) / 1e9 if trace_ms else None
+    return {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak if achieved else None,
+            "peak_source": f"nominal: 128 B/clk/SM x {sms} SMs x {mhz:.0f} MHz",
+            "note": "d=1 reads 24 B/point-step (A,B,C cell polynomial) against the 32 B algorithmic figure; "
+                    "random late-time gathers cost ~3.75 wavefronts per 8-byte warp load (ncu, profiles/)"}
+
+
 def flush_l2(torch, buf):
     buf.add_(1.0)  # 256 MiB write > 126 MB L2
 
@@ -276,7 +297,10 @@ def gpu_arm(args, rank: int, world: int):
                    else f"trace_rho_kernel<{g.d}>"), "algo_flops_per_point_step": ALGO_FLOPS[g.d],
         "trace_launches": int(trace_launches), "trace_ms_per_launch": trace_ms / max(1, trace_launches),
         "trace_share_of_run": trace_ms / (trace_ms + reduce_ms + field_ms) if trace_ms else None,
+        "reduce_ms_per_launch": reduce_ms / reduce_launches if reduce_launches else None,
+        "field_ms_per_launch": field_ms / field_launches if field_launches else None,
         "peak_source": "measured in-run: DFMA-chain kernel (nufi_fp64_peak); MEASURED_PEAKS.json has no FP64 entry",
+        "secondary": smem_roofline(torch, dev, g.d, trace_ps, trace_ms),
         "note": "tensor cores not applicable (FP64 gather-stencil, no dense contraction); HBM ~0 (history L2-resident)",
     }
 

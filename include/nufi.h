@@ -135,6 +135,15 @@ int nufi_rho_partials(nufi_handle *h, int64_t n, double *partials, int64_t *eval
  * Every rank runs it redundantly and so holds the full history. */
 int nufi_step_finish(nufi_handle *h, int64_t n, const double *partials, double *rho_out, double *E_out,
                      double *W_out, double *stats3);
+/* Stream-ordered variant of nufi_step_finish for a host loop that enqueues a whole
+ * run ahead (trace -> allreduce -> finish per step, no host synchronisation):
+ * outputs must be DEVICE buffers (or NULL); a failing step (non-neutral rho) sets
+ * a device flag that makes every later field update a no-op.  Call
+ * nufi_check_status() at the end: NUFI_ERR_NUMERICAL if any step failed (the
+ * history length is then reset to the fields actually appended). */
+int nufi_step_finish_async(nufi_handle *h, int64_t n, const double *partials, double *rho_out, double *E_out,
+                           double *W_out, double *stats3);
+int nufi_check_status(nufi_handle *h);
 /* Fixed-order combine of the (allreduced) block partials -> rho, stats3. */
 int nufi_rho_finish(nufi_handle *h, const double *partials, double *rho_out, double *stats3);
 int64_t nufi_partials_len(nufi_handle *h); /* v_blocks * (Nx^d + 2) */

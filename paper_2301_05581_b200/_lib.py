@@ -90,6 +90,8 @@ _SIGS = {
     "nufi_rho_partials": [_P, _I64, _P, _I64P],
     "nufi_rho_finish": [_P, _P, _P, _P],
     "nufi_step_finish": [_P, _I64, _P, _P, _P, _P, _P],
+    "nufi_step_finish_async": [_P, _I64, _P, _P, _P, _P, _P],
+    "nufi_check_status": [_P],
     "nufi_partials_len": [_P],
     "nufi_field_update": [_P, _P, _P, _P, _P],
     "nufi_step": [_P, _I64, _P, _P, _P, _P, _I64P],

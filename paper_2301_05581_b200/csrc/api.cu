@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -150,6 +152,55 @@ static bool is_device_ptr(const void *p) {
         return false;
     }
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// ---- memory: stream-ordered device allocations from the device's default pool
+// (retained across handles: release threshold = max), pinned host staging from a
+// process-wide cache.  Creating and destroying a handle per run (the public
+// Simulation(...).run() call) then costs no cudaMalloc / cudaFree / page pinning,
+// each of which synchronises the device or the OS (measured 25-275 ms per destroy).
+static cudaError_t pool_init(int device) {
+    static bool done[64] = {false};
+    if (device < 0 || device >= 64 || done[device]) return cudaSuccess;
+    cudaMemPool_t pool;
+    cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, device);
+    if (e != cudaSuccess) return e;
+    uint64_t thr = UINT64_MAX;
+    e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    if (e == cudaSuccess) done[device] = true;
+    return e;
+}
+
+template <typename T>
+static cudaError_t dalloc(T **p, size_t bytes, cudaStream_t st) {
+    return cudaMallocAsync(reinterpret_cast<void **>(p), bytes ? bytes : 8, st);
+}
+
+struct PinnedCache {
+    std::mutex mu;
+    std::vector<std::pair<size_t, double *>> free_blocks;
+};
+static PinnedCache &pinned_cache() {
+    static PinnedCache *c = new PinnedCache();  // never destroyed: no teardown-order issues
+    return *c;
+}
+static cudaError_t pinned_get(double **p, size_t elems) {
+    {
+        std::lock_guard<std::mutex> lk(pinned_cache().mu);
+        auto &v = pinned_cache().free_blocks;
+        for (size_t i = 0; i < v.size(); ++i)
+            if (v[i].first >= elems) {
+                *p = v[i].second;
+                v.erase(v.begin() + i);
+                return cudaSuccess;
+            }
+    }
+    return cudaMallocHost(reinterpret_cast<void **>(p), elems * sizeof(double));
+}
+static void pinned_put(double *p, size_t elems) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(pinned_cache().mu);
+    pinned_cache().free_blocks.push_back({elems, p});
 }
 
 static int ipow(int b, int e) {
@@ -308,8 +359,8 @@ static int install_ic(nufi_handle *h, const nufi_config &c) {
 static int grow(nufi_handle *h, int64_t cap) {
     if (cap <= h->cap) return NUFI_OK;
     double *nh = nullptr, *ne = nullptr;
-    CU(cudaMalloc(&nh, cap * (size_t)h->nodes * sizeof(double)));
-    CU(cudaMalloc(&ne, cap * (size_t)h->ev_elems * sizeof(double)));
+    CU(dalloc(&nh, cap * (size_t)h->nodes * sizeof(double), h->stream));
+    CU(dalloc(&ne, cap * (size_t)h->ev_elems * sizeof(double), h->stream));
     if (h->len > 0) {
         CU(cudaMemcpyAsync(nh, h->hist, h->len * (size_t)h->nodes * sizeof(double), cudaMemcpyDeviceToDevice,
                            h->stream));
@@ -317,8 +368,8 @@ static int grow(nufi_handle *h, int64_t cap) {
                            h->stream));
     }
     CU(cudaStreamSynchronize(h->stream));
-    cudaFree(h->hist);
-    cudaFree(h->ev_hist);
+    cudaFreeAsync(h->hist, h->stream);
+    cudaFreeAsync(h->ev_hist, h->stream);
     h->hist = nh;
     h->ev_hist = ne;
     h->cap = cap;
@@ -412,22 +463,23 @@ int nufi_create(const nufi_config *cfg, int device, void *stream, nufi_handle **
     choose_tiling(h);
 
     const size_t nodes = h->nodes;
-    CU(cudaMalloc(&h->hist, h->cap * nodes * sizeof(double)));
-    CU(cudaMalloc(&h->ev_hist, h->cap * (size_t)h->ev_elems * sizeof(double)));
+    CU(pool_init(device));
+    CU(dalloc(&h->hist, h->cap * nodes * sizeof(double), h->stream));
+    CU(dalloc(&h->ev_hist, h->cap * (size_t)h->ev_elems * sizeof(double), h->stream));
     // x2: the persistent d = 1 run kernel double-buffers the tile partials by step parity
-    CU(cudaMalloc(&h->partial, 2 * (size_t)h->vt_total * h->node_tiles * 32 * sizeof(double)));
-    CU(cudaMalloc(&h->fminmax, 2 * (size_t)h->vt_total * h->node_tiles * 2 * sizeof(double)));
-    CU(cudaMalloc(&h->blocks, ((size_t)h->B * nodes + 2 * h->B) * sizeof(double)));
-    CU(cudaMalloc(&h->d_rho, nodes * sizeof(double)));
-    CU(cudaMalloc(&h->d_E, nodes * c.d * sizeof(double)));
-    CU(cudaMalloc(&h->d_W, 8 * sizeof(double)));
-    CU(cudaMalloc(&h->d_stats, 8 * sizeof(double)));
-    CU(cudaMalloc(&h->d_rho_bar, sizeof(double)));
-    CU(cudaMalloc(&h->d_status, sizeof(int)));
-    CU(cudaMalloc(&h->d_len, sizeof(int64_t)));
-    CU(cudaMalloc(&h->tables, (4 * (size_t)h->N + 3 * nodes) * sizeof(double)));
-    CU(cudaMalloc(&h->ticket, sizeof(unsigned)));
-    CU(cudaMalloc(&h->barrier, sizeof(unsigned)));
+    CU(dalloc(&h->partial, 2 * (size_t)h->vt_total * h->node_tiles * 32 * sizeof(double), h->stream));
+    CU(dalloc(&h->fminmax, 2 * (size_t)h->vt_total * h->node_tiles * 2 * sizeof(double), h->stream));
+    CU(dalloc(&h->blocks, ((size_t)h->B * nodes + 2 * h->B) * sizeof(double), h->stream));
+    CU(dalloc(&h->d_rho, nodes * sizeof(double), h->stream));
+    CU(dalloc(&h->d_E, nodes * c.d * sizeof(double), h->stream));
+    CU(dalloc(&h->d_W, 8 * sizeof(double), h->stream));
+    CU(dalloc(&h->d_stats, 8 * sizeof(double), h->stream));
+    CU(dalloc(&h->d_rho_bar, sizeof(double), h->stream));
+    CU(dalloc(&h->d_status, sizeof(int), h->stream));
+    CU(dalloc(&h->d_len, sizeof(int64_t), h->stream));
+    CU(dalloc(&h->tables, (4 * (size_t)h->N + 3 * nodes) * sizeof(double), h->stream));
+    CU(dalloc(&h->ticket, sizeof(unsigned), h->stream));
+    CU(dalloc(&h->barrier, sizeof(unsigned), h->stream));
     CU(cudaMemsetAsync(h->ticket, 0, sizeof(unsigned), h->stream));
     CU(launch_field_tables(h->tables, h->tables + 2 * h->N, h->tables + 2 * h->N + 2 * nodes, c.d, c.Nx, h->nodes,
                            2.0 * M_PI / c.L, h->stream));
@@ -451,8 +503,9 @@ int nufi_destroy(nufi_handle *h) {
                     (void *)h->d_rho, (void *)h->d_E, (void *)h->d_W, (void *)h->d_stats, (void *)h->d_rho_bar,
                     (void *)h->d_status, (void *)h->d_len, (void *)h->run_dev, (void *)h->tables,
                     (void *)h->ticket, (void *)h->barrier, (void *)h->mom_part, (void *)h->d_mom})
-        if (p) cudaFree(p);
-    if (h->run_host) cudaFreeHost(h->run_host);
+        if (p) cudaFreeAsync(p, h->stream);
+    cudaStreamSynchronize(h->stream);  // frees complete -> the pool can hand the memory to the next handle
+    pinned_put(h->run_host, h->run_elems);
     if (h->own_stream) cudaStreamDestroy(h->stream);
     delete h;
     return NUFI_OK;
@@ -806,6 +859,48 @@ int nufi_step_finish(nufi_handle *h, int64_t n, const double *partials, double *
     return copy_step_outputs(h, rho_out, E_out, W_out, stats3);
 }
 
+int nufi_step_finish_async(nufi_handle *h, int64_t n, const double *partials, double *rho_out, double *E_out,
+                           double *W_out, double *stats3) {
+    CHECK_HANDLE(h);
+    if (n != h->len) return fail(NUFI_ERR_USAGE, "step_finish requires len == n");
+    if (n >= h->cap) return fail(NUFI_ERR_USAGE, "history is full (capacity n_max + 1)");
+    for (const void *q : {(const void *)partials, (const void *)rho_out, (const void *)E_out, (const void *)W_out,
+                          (const void *)stats3})
+        if (q && !is_device_ptr(q)) return fail(NUFI_ERR_USAGE, "async step outputs must be device buffers");
+    if (!partials) return fail(NUFI_ERR_USAGE, "null partials");
+    FieldParams f = field_params(h);
+    f.sums = partials;
+    f.rows_per_block = 1;
+    f.minmax = partials + (size_t)h->B * h->nodes;
+    f.mm_per_block = 1;
+    f.slot = n;
+    f.rho_out = rho_out;
+    f.stats_out = stats3;
+    f.W_out = W_out;
+    f.E_out = E_out;
+    {
+        ProfScope ps(h, 2);
+        CU(launch_field_update(f, h->stream));
+    }
+    h->len += 1;  // provisional; nufi_check_status() reconciles with the device length
+    return NUFI_OK;
+}
+
+int nufi_check_status(nufi_handle *h) {
+    CHECK_HANDLE(h);
+    int st = 0;
+    int64_t dlen = 0;
+    CU(cudaMemcpyAsync(&st, h->d_status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaMemcpyAsync(&dlen, h->d_len, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    if (st == NUFI_ERR_NUMERICAL) {
+        h->len = dlen;  // the fields actually appended before the failing step
+        CU(cudaMemsetAsync(h->d_status, 0, sizeof(int), h->stream));
+        return fail(NUFI_ERR_NUMERICAL, "solve_poisson: density is not neutral: nodal mean exceeds 1e-8 max|rho|");
+    }
+    return NUFI_OK;
+}
+
 int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, double *W_hist, double *stats_hist,
              int64_t *evals) {
     CHECK_HANDLE(h);
@@ -820,12 +915,12 @@ int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, d
                          is_device_ptr(stats_hist)};
     const size_t need = (size_t)steps * per_step;
     if (need > h->run_elems) {
-        if (h->run_dev) cudaFree(h->run_dev);
-        if (h->run_host) cudaFreeHost(h->run_host);
+        if (h->run_dev) cudaFreeAsync(h->run_dev, h->stream);
+        pinned_put(h->run_host, h->run_elems);
         h->run_dev = nullptr;
         h->run_host = nullptr;
-        CU(cudaMalloc(&h->run_dev, need * sizeof(double)));
-        CU(cudaMallocHost(&h->run_host, need * sizeof(double)));
+        CU(dalloc(&h->run_dev, need * sizeof(double), h->stream));
+        CU(pinned_get(&h->run_host, need));
         h->run_elems = need;
     }
     double *base_dev[4] = {h->run_dev, h->run_dev + steps * nodes, h->run_dev + steps * (nodes + nodes * d),
@@ -1002,8 +1097,8 @@ int nufi_moments(nufi_handle *h, int64_t n, double *out, int64_t *evals) {
     const int nm = mom_sums(h->d) + 2;
     const int ctas = (h->b_hi - h->b_lo) * h->vt_per_block * h->node_tiles;
     if (!h->mom_part) {
-        CU(cudaMalloc(&h->mom_part, (size_t)h->vt_total * h->node_tiles * nm * sizeof(double)));
-        CU(cudaMalloc(&h->d_mom, 16 * sizeof(double)));
+        CU(dalloc(&h->mom_part, (size_t)h->vt_total * h->node_tiles * nm * sizeof(double), h->stream));
+        CU(dalloc(&h->d_mom, 16 * sizeof(double), h->stream));
     }
     TraceRhoParams p = trace_params(h, n, h->b_lo);
     p.partial = h->mom_part;

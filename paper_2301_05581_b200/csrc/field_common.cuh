@@ -166,8 +166,10 @@ __device__ __forceinline__ void dft_pass(const double *__restrict__ ire, const d
 static __device__ __forceinline__ void circulant_direct(const double *gc, const double *gp, const double *r, double *c,
                                                         double *phi, int N) {
     const int T = blockDim.x;
-    int G = 1;
-    while (G < 32 && 2 * G <= N && 2 * N * (2 * G) <= T) G *= 2;
+    // lanes per output from N alone (the values the old T = 256 / 288 rule gave), so
+    // the summation order -- and the bits -- never depend on the CTA size
+    int G = 128 / N < N / 2 ? 128 / N : N / 2;
+    G = G < 1 ? 1 : (G > 32 ? 32 : G);
     const int part = threadIdx.x % G;
     for (int base = 0; base < 2 * N; base += T / G) {  // warp-uniform trip count
         const int o = base + threadIdx.x / G;

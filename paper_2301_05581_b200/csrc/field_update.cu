@@ -12,6 +12,9 @@ namespace nufi {
 
 __global__ void __launch_bounds__(1024) field_update_kernel(const FieldParams p) {
     extern __shared__ __align__(16) double fsm[];
+    // an earlier step of an asynchronously enqueued sequence failed (non-neutral rho):
+    // leave the history untouched, like the reference which raises before appending
+    if (p.status && *(volatile int *)p.status != 0) return;
     field_update_body(p, fsm);
 }
 

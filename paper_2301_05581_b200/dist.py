@@ -98,7 +98,7 @@ class DistributedSimulation:
         self.partials = torch.zeros(n, dtype=torch.float64, device=f"cuda:{device}")
         self.block_lo, self.block_hi = lo, hi
 
-    def step(self, outputs: dict | None = None, row: int = 0):
+    def step(self, outputs: dict | None = None, row: int = 0, sync: bool = True):
         """One step: trace own blocks -> allreduce -> redundant field update."""
         h = self.history.handle
         n = len(self.history)
@@ -114,13 +114,23 @@ class DistributedSimulation:
             return a.data_ptr() + row * width * 8 if hasattr(a, "data_ptr") else a.ctypes.data + row * width * 8
 
         g = self.grid
-        h.call("nufi_step_finish", n, self.partials.data_ptr(), rowptr("rho", g.n_nodes),
-               rowptr("E", g.n_nodes * g.d), rowptr("W", 1), rowptr("stats", 3))
+        args = (n, self.partials.data_ptr(), rowptr("rho", g.n_nodes), rowptr("E", g.n_nodes * g.d),
+                rowptr("W", 1), rowptr("stats", 3))
+        if sync:
+            h.call("nufi_step_finish", *args)
+        else:
+            h.call("nufi_step_finish_async", *args)  # stream-ordered, device outputs
         self.ctx.field_evals += int(ev.value)
         return n
 
     def run(self, outputs: dict | None = None):
+        """The whole loop.  With device (CUDA tensor) outputs, or none, every step is
+        enqueued without a host synchronisation (trace -> NCCL allreduce -> field
+        update, all on one stream); the status is checked once at the end."""
         first = len(self.history)
+        dev = all(v is None or hasattr(v, "data_ptr") for v in (outputs or {}).values())
         for n in range(first, self.n_steps + 1):
-            self.step(outputs, n - first)
+            self.step(outputs, n - first, sync=not dev)
+        if dev:
+            self.history.handle.call("nufi_check_status")
         return outputs

@@ -22,7 +22,7 @@ from paper_2301_05581_b200.dist import block_range
 pytestmark = pytest.mark.gpu
 
 
-def sharded_run(name, N, world, B=8):
+def sharded_run(name, N, world, B=8, asynchronous=False):
     w = workload(name)
     g = w.grid
     ranks = []
@@ -43,12 +43,24 @@ def sharded_run(name, N, world, B=8):
         table = sum(p for _, p in ranks)  # the allreduce
         torch.cuda.synchronize()
         for r, (h, _) in enumerate(ranks):
-            out_rho = np.empty(g.n_nodes)
-            out_W = np.empty(1)
-            h.handle.call("nufi_step_finish", n, table.data_ptr(), out_rho.ctypes.data, None, out_W.ctypes.data,
-                          None)
-            rho[r, n] = out_rho
-            W[r, n] = out_W[0]
+            if asynchronous:  # device outputs, stream-ordered (DistributedSimulation.run)
+                d_rho = torch.empty(g.n_nodes, dtype=torch.float64, device="cuda")
+                d_W = torch.empty(1, dtype=torch.float64, device="cuda")
+                h.handle.call("nufi_step_finish_async", n, table.data_ptr(), d_rho.data_ptr(), None,
+                              d_W.data_ptr(), None)
+                h.handle.call("nufi_sync")
+                rho[r, n] = d_rho.cpu().numpy()
+                W[r, n] = float(d_W[0])
+            else:
+                out_rho = np.empty(g.n_nodes)
+                out_W = np.empty(1)
+                h.handle.call("nufi_step_finish", n, table.data_ptr(), out_rho.ctypes.data, None,
+                              out_W.ctypes.data, None)
+                rho[r, n] = out_rho
+                W[r, n] = out_W[0]
+    if asynchronous:
+        for h, _ in ranks:
+            h.handle.call("nufi_check_status")
     hists = [h.stacked().reshape(N + 1, -1) for h, _ in ranks]
     return rho, W, hists, evals
 
@@ -66,3 +78,13 @@ def test_sharded_bit_identical_to_single_gpu(name, N, world):
         assert np.array_equal(W[r], ref.W)
         assert np.array_equal(hists[r], ref_hist)
     assert evals == ref.field_evals
+
+
+@pytest.mark.parametrize("name,N", [("kat_wl", 30), ("tiny2", 10)])
+def test_sharded_async_finish_bit_identical(name, N):
+    w = workload(name)
+    ref = nufi.Simulation(w.grid, w.ic, w.tau, N, v_blocks=8).run()
+    rho, W, hists, _ = sharded_run(name, N, 2, asynchronous=True)
+    for r in range(2):
+        assert np.array_equal(rho[r], ref.rho) and np.array_equal(W[r], ref.W)
+
