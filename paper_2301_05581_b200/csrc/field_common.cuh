@@ -268,24 +268,49 @@ static __device__ __forceinline__ bool field_update_1d_body(const FieldParams &p
     // ---- block sums over the block's rows in order (reduce_blocks_kernel order) ----
     double mn = DBL_MAX, mx = -DBL_MAX;
     if (p.sums) {
-        for (int it = threadIdx.x; it < B * N; it += T) {
-            const int b = it / N, i = it - b * N;
-            const double *src = p.sums + (size_t)b * rpb * N + i;
-            double Sb = 0.0;
-            int q = 0;
-            for (; q + 8 <= rpb; q += 8) {
-                double v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (size_t)(q + u) * N);
-#pragma unroll
-                for (int u = 0; u < 8; ++u) Sb += v[u];
-            }
-            for (; q < rpb; ++q) Sb += __ldcg(src + (size_t)q * N);
-            sb[it] = Sb;
-        }
         for (int q = threadIdx.x; q < B * p.mm_per_block; q += T) {
             mn = fmin(mn, __ldcg(p.minmax + 2 * q));
             mx = fmax(mx, __ldcg(p.minmax + 2 * q + 1));
+        }
+        if (rpb <= 8) {
+            // two outputs per thread per pass: all 2 * rpb loads in flight at once (one L2
+            // round trip instead of two on the latency-critical path); same order as below
+            for (int it = threadIdx.x; it < B * N; it += 2 * T) {
+                const int it2 = it + T;
+                const double *s1 = p.sums + (size_t)(it / N) * rpb * N + (it % N);
+                const double *s2 = p.sums + (size_t)(it2 / N) * rpb * N + (it2 % N);
+                double v1[8], v2[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    v1[u] = u < rpb ? __ldcg(s1 + (size_t)u * N) : 0.0;
+                    v2[u] = (u < rpb && it2 < B * N) ? __ldcg(s2 + (size_t)u * N) : 0.0;
+                }
+                double S1 = 0.0, S2 = 0.0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (u < rpb) {
+                        S1 += v1[u];
+                        S2 += v2[u];
+                    }
+                sb[it] = S1;
+                if (it2 < B * N) sb[it2] = S2;
+            }
+        } else {
+            for (int it = threadIdx.x; it < B * N; it += T) {
+                const int b = it / N, i = it - b * N;
+                const double *src = p.sums + (size_t)b * rpb * N + i;
+                double Sb = 0.0;
+                int q = 0;
+                for (; q + 8 <= rpb; q += 8) {
+                    double v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (size_t)(q + u) * N);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) Sb += v[u];
+                }
+                for (; q < rpb; ++q) Sb += __ldcg(src + (size_t)q * N);
+                sb[it] = Sb;
+            }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -309,33 +334,33 @@ static __device__ __forceinline__ bool field_update_1d_body(const FieldParams &p
             r[i] = p.rho_bar - p.hv_d * S;
         }
     __syncthreads();
-    if (warp == 0) {
+    // every warp forms the mean itself (identical order in every warp: no barrier and
+    // no shared-memory round trip), the neutral rho goes to the free block-sum array
+    double neut;
+    {
         double s = 0.0;
         for (int i = lane; i < N; i += 32) s += r[i];
         s = warp_sum(s);
+        neut = p.sums ? s / (double)N : 0.0;  // density.py:84
+    }
+    if (threadIdx.x == 0 && p.stats_out) {
         double fmn = DBL_MAX, fmx = -DBL_MAX;
         if (p.sums)
             for (int w = 0; w < (T >> 5); ++w) {
                 fmn = fmin(fmn, scratch[w]);
                 fmx = fmax(fmx, scratch[32 + w]);
             }
-        if (lane == 0) {
-            const double neut = p.sums ? s / (double)N : 0.0;  // density.py:84
-            scratch[0] = neut;
-            if (p.stats_out) {
-                p.stats_out[0] = neut;
-                p.stats_out[1] = fmn;
-                p.stats_out[2] = fmx;
-            }
-        }
+        p.stats_out[0] = neut;
+        p.stats_out[1] = fmn;
+        p.stats_out[2] = fmx;
     }
-    __syncthreads();
-    const double neut = scratch[0];
+    double *rn = sb;  // B * N >= N doubles, no longer needed
     for (int i = threadIdx.x; i < N; i += T) {
         const double v = r[i] - neut;  // density.py:85
-        r[i] = v;
+        rn[i] = v;
         if (p.rho_out) p.rho_out[i] = v;
     }
+    r = rn;
     if (p.finish_only) return true;
     __syncthreads();
     NUFI_STAMP(p, 2);

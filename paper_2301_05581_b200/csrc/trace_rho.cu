@@ -245,48 +245,48 @@ __global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams 
 // of this rank's blocks; CTA 0 additionally reduces the min / max.
 __global__ void reduce_blocks_kernel(const double *__restrict__ partial, const double *__restrict__ fminmax,
                                      double *__restrict__ out, int nodes, int node_tiles, int vt_per_block,
-                                     int b_lo, int b_hi, int B) {
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t count = (int64_t)(b_hi - b_lo) * nodes;
-    if (tid < count) {
-        const int b = b_lo + (int)(tid / nodes);
-        const int node = (int)(tid % nodes);
-        const double *src = partial + (size_t)b * vt_per_block * nodes + node;
-        double s = 0.0;
-        for (int t = 0; t < vt_per_block; ++t) s += src[(size_t)t * nodes];
-        out[(size_t)b * nodes + node] = s;
-    }
-    if (blockIdx.x == 0) {
-        double *mm = out + (size_t)B * nodes;
-        for (int b = b_lo; b < b_hi; ++b) {
-            double mn = DBL_MAX, mx = -DBL_MAX;
-            const int64_t c0 = (int64_t)b * vt_per_block * node_tiles;
-            const int64_t c1 = c0 + (int64_t)vt_per_block * node_tiles;
-            for (int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
-                mn = fmin(mn, fminmax[2 * c]);
-                mx = fmax(mx, fminmax[2 * c + 1]);
-            }
-            __shared__ double smn[32], smx[32];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            }
-            if ((threadIdx.x & 31) == 0) {
-                smn[threadIdx.x >> 5] = mn;
-                smx[threadIdx.x >> 5] = mx;
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-                    mn = fmin(mn, smn[w]);
-                    mx = fmax(mx, smx[w]);
-                }
-                mm[2 * b] = mn;
-                mm[2 * b + 1] = mx;
-            }
-            __syncthreads();
+                                     int b_lo, int b_hi, int B, int sum_ctas) {
+    if ((int)blockIdx.x < sum_ctas) {
+        const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        const int64_t count = (int64_t)(b_hi - b_lo) * nodes;
+        if (tid < count) {
+            const int b = b_lo + (int)(tid / nodes);
+            const int node = (int)(tid % nodes);
+            const double *src = partial + (size_t)b * vt_per_block * nodes + node;
+            double s = 0.0;
+            for (int t = 0; t < vt_per_block; ++t) s += src[(size_t)t * nodes];
+            out[(size_t)b * nodes + node] = s;
         }
+        return;
+    }
+    // one CTA per block of this rank: (min, max) over the block's tile pairs
+    const int b = b_lo + (int)blockIdx.x - sum_ctas;
+    double *mm = out + (size_t)B * nodes;
+    double mn = DBL_MAX, mx = -DBL_MAX;
+    const int64_t c0 = (int64_t)b * vt_per_block * node_tiles;
+    const int64_t c1 = c0 + (int64_t)vt_per_block * node_tiles;
+    for (int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+        mn = fmin(mn, fminmax[2 * c]);
+        mx = fmax(mx, fminmax[2 * c + 1]);
+    }
+    __shared__ double smn[32], smx[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        smn[threadIdx.x >> 5] = mn;
+        smx[threadIdx.x >> 5] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            mn = fmin(mn, smn[w]);
+            mx = fmax(mx, smx[w]);
+        }
+        mm[2 * b] = mn;
+        mm[2 * b + 1] = mx;
     }
 }
 
@@ -384,9 +384,9 @@ cudaError_t launch_reduce_blocks(const double *partial, const double *fminmax, d
                                  int node_tiles, int vt_per_block, int b_lo, int b_hi, int B, cudaStream_t st) {
     const int64_t count = (int64_t)(b_hi - b_lo) * nodes;
     const int threads = 256;
-    const int ctas = (int)std::max<int64_t>(1, (count + threads - 1) / threads);
-    reduce_blocks_kernel<<<ctas, threads, 0, st>>>(partial, fminmax, out, nodes, node_tiles, vt_per_block, b_lo,
-                                                   b_hi, B);
+    const int sum_ctas = (int)((count + threads - 1) / threads);
+    reduce_blocks_kernel<<<sum_ctas + (b_hi - b_lo), threads, 0, st>>>(partial, fminmax, out, nodes, node_tiles,
+                                                                       vt_per_block, b_lo, b_hi, B, sum_ctas);
     return cudaGetLastError();
 }
 

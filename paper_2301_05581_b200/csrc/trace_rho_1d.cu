@@ -17,6 +17,7 @@
 // immediates.  Slab 0 is stored pre-halved, so the final tau/2 kick needs no
 // special case.
 #include <cfloat>
+#include <cstdlib>
 
 #include "field_common.cuh"
 
@@ -192,7 +193,13 @@ size_t trace_rho_1d_smem_bytes(const TraceRhoParams &p, int threads, int nodes) 
 int trace_rho_1d_sps(int N) {
     if (N == 32 || N == 64) return 16;
     if (N == 128) return 8;
-    if (N == 256) return 4;
+    if (N == 256) {
+        if (const char *e = getenv("NUFI_D1_SPS")) {
+            const int v = atoi(e);
+            if (v == 1 || v == 2 || v == 4) return v;
+        }
+        return 4;
+    }
     return 1;
 }
 
@@ -213,7 +220,10 @@ cudaError_t launch_trace_rho_1d(const TraceRhoParams &p, const FieldParams &fp, 
         case 32: return launch1<32, 16>(p, fp, fuse, ticket, ctas, threads, smem, st);
         case 64: return launch1<64, 16>(p, fp, fuse, ticket, ctas, threads, smem, st);
         case 128: return launch1<128, 8>(p, fp, fuse, ticket, ctas, threads, smem, st);
-        case 256: return launch1<256, 4>(p, fp, fuse, ticket, ctas, threads, smem, st);
+        case 256:
+            if (p.slabs_per_stage == 1) return launch1<256, 1>(p, fp, fuse, ticket, ctas, threads, smem, st);
+            if (p.slabs_per_stage == 2) return launch1<256, 2>(p, fp, fuse, ticket, ctas, threads, smem, st);
+            return launch1<256, 4>(p, fp, fuse, ticket, ctas, threads, smem, st);
         default: return launch1<0, 1>(p, fp, fuse, ticket, ctas, threads, smem, st);
     }
 }

@@ -29,4 +29,11 @@ print(f"{name}: steps {len(rows)} total {tot / 1e3:.2f} ms | trace {trace.sum() 
 for q in (10, 100, 400, 800, 1200, len(rows) - 1):
     if q < len(rows) - 1:
         print(f"  n={q}: trace {trace[q - 1] / 1e3:.1f} us barrier {barrier[q] / 1e3:.1f} us tail {tail[q] / 1e3:.1f} us")
-print("".join(l for l in open(path) if l.startswith("#"))[:3000])
+for l in open(path):
+    if l.startswith("# tail phases"):
+        print(l.strip())
+    if l.startswith("# wait/total"):
+        pairs = [tuple(map(int, x.split("/"))) for x in l.split(":")[1].split()]
+        w = np.array([a for a, b in pairs], float)
+        t = np.array([b for a, b in pairs], float)
+        print(f"  TMA wait share of the trace (last step, per CTA): mean {np.mean(w / t):.3f} max {np.max(w / t):.3f}")
