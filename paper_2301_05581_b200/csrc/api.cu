@@ -298,7 +298,7 @@ static void choose_tiling(nufi_handle *h) {
     const int slab_bytes = h->ev_elems * 8;
     if (h->d == 1) {
         h->sps = trace_rho_1d_sps(h->N);  // must match the kernel's template instantiation
-        h->stages = h->N >= 256 ? 2 : 4;  // 2 CTAs / SM for the large-N (throughput-bound) case
+        h->stages = 4;  // 2 CTAs / SM still fit for N = 256 (the tail workspace aliases the ring)
         if (const char *e = getenv("NUFI_D1_STAGES")) h->stages = std::max(2, atoi(e));
     } else if (h->d == 2) {
         h->sps = std::max(1, 40960 / slab_bytes);  // ~40 KB stages, 2-deep ring: 2 CTAs / SM

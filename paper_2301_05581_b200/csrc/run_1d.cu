@@ -61,6 +61,12 @@ __device__ __forceinline__ void kick1_any(double &X, double &V, const double *__
     V = fma(fc, t, V + A);
 }
 
+// doubles of the ring / tail-workspace union (16-byte aligned end for the barriers)
+__host__ __device__ inline size_t run_1d_ring_doubles(int stages, int sps, int slab, int nodes, int N) {
+    const size_t ring = (size_t)stages * sps * slab, tail = (size_t)field_smem_doubles(nodes, N, true);
+    return ((ring > tail ? ring : tail) + 1) & ~(size_t)1;
+}
+
 template <int NX, int SPS>
 __global__ void __launch_bounds__(288, 2) run_1d_kernel(const Run1DParams P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -73,13 +79,17 @@ __global__ void __launch_bounds__(288, 2) run_1d_kernel(const Run1DParams P) {
     const int stages = p.stages;
     const int nodes = p.nodes;
 
-    // shared memory: ring | barriers | red | local slab | tail workspace
+    // shared memory: [ring | tail workspace (aliased)] | barriers | red | local slab.
+    // The tail runs between grid barriers when no bulk copy is in flight (every copy
+    // of a step is consumed before its barrier), so it reuses the ring's bytes;
+    // the ring is re-armed behind a proxy fence (generic writes -> async-proxy writes).
+    const size_t ring_doubles = run_1d_ring_doubles(stages, SPS, SLAB, nodes, N);
     double *ring = reinterpret_cast<double *>(smem_raw);
-    uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)stages * SPS * SLAB);
+    double *tail = ring;                                                   // field_smem_doubles(nodes, N, true)
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + ring_doubles);
     uint64_t *empty = full + stages;
     double *red = reinterpret_cast<double *>(empty + stages);  // 3 * 32 * cw
     double *slabN = red + 3 * 32 * cw;                          // evaluation slab n-1 (SLAB)
-    double *tail = slabN + SLAB;                                // field_smem_doubles(nodes, N, true)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
@@ -297,6 +307,9 @@ __global__ void __launch_bounds__(288, 2) run_1d_kernel(const Run1DParams P) {
         fp.tstamps = (P.stamps && blockIdx.x == 0 && n == P.n_last) ? P.stamps + 3 * (P.n_last - P.n_first + 1) : nullptr;
         const bool ok = field_update_body(fp, tail);
         __syncthreads();
+        // the tail's generic-proxy writes to the ring bytes must be ordered before the
+        // next step's bulk copies (async proxy) into them
+        if (producer && lane == 0) fence_proxy_async_smem();
         if (P.stamps && blockIdx.x == 0 && threadIdx.x == 0) P.stamps[3 * (n - P.n_first) + 2] = globaltimer();
         if (!ok) break;  // identical decision in every CTA
     }
@@ -304,8 +317,8 @@ __global__ void __launch_bounds__(288, 2) run_1d_kernel(const Run1DParams P) {
 
 size_t run_1d_smem_bytes(const TraceRhoParams &p, int threads) {
     const int cw = threads / 32 - 1;
-    return (size_t)p.stages * p.slabs_per_stage * p.ev_slab_elems * sizeof(double) + 2 * p.stages * sizeof(uint64_t) +
-           (3 * 32 * (size_t)cw + p.ev_slab_elems + field_smem_doubles(p.nodes, p.N, true)) * sizeof(double);
+    return run_1d_ring_doubles(p.stages, p.slabs_per_stage, p.ev_slab_elems, p.nodes, p.N) * sizeof(double) +
+           2 * p.stages * sizeof(uint64_t) + (3 * 32 * (size_t)cw + p.ev_slab_elems) * sizeof(double);
 }
 
 template <int NX, int SPS>
