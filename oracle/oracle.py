@@ -105,6 +105,12 @@ def case(name: str) -> Case:
     if name == "tiny3":
         streams = Profile(centers=(-2.4, 2.4), weights=(0.5, 0.5))
         return Case(3, 10.0 * math.pi, 8, 4, 6.0, 1 / 8, 1e-3, 0.2, (_MAX, streams, _MAX))
+    if name == "rag1":
+        return Case(1, FOUR_PI, 24, 40, 6.0, 1 / 8, 0.05, 0.5, (_MAX,))
+    if name == "rag2":
+        return Case(2, FOUR_PI, 6, 10, 6.0, 1 / 8, 0.3, 0.5, (_MAX,) * 2)
+    if name == "rag3":
+        return Case(3, FOUR_PI, 5, 3, 5.0, 1 / 8, 0.05, 0.5, (_MAX,) * 3)
     raise KeyError(name)
 
 

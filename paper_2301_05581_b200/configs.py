@@ -59,11 +59,21 @@ def workload(name: str) -> Workload:
     if name == "tiny3":
         return Workload(name, GridSpec(3, 10.0 * math.pi, 8, 4, 6.0), make_benchmark("two_stream_3d"), 1 / 8, 12,
                         "d=3 two-stream 8^3 x 4^3")
+    # ragged / non-power-of-two grids (generic-N paths)
+    if name == "rag1":
+        return Workload(name, GridSpec(1, FOUR_PI, 24, 40, 6.0), make_benchmark("weak_landau_1d", alpha=0.05), 1 / 8,
+                        40, "d=1 weak Landau, Nx=24 (non-power-of-two), Nv=40")
+    if name == "rag2":
+        return Workload(name, GridSpec(2, FOUR_PI, 6, 10, 6.0), make_benchmark("strong_landau_2d", alpha=0.3), 1 / 8,
+                        16, "d=2 Landau, 6^2 x 10^2")
+    if name == "rag3":
+        return Workload(name, GridSpec(3, FOUR_PI, 5, 3, 5.0), weak_landau_3d(alpha=0.05), 1 / 8, 8,
+                        "d=3 Landau, 5^3 x 3^3")
     raise KeyError(name)
 
 
 BASELINE = ("wl1", "ts1", "sl1", "wl2", "wl3")
-PARITY_CASES = ("kat_wl", "eq1", "tiny2", "tiny3", "wl3r")
+PARITY_CASES = ("kat_wl", "eq1", "tiny2", "tiny3", "wl3r", "rag1", "rag2", "rag3")
 
 # flops per point-step counted on the reference's arithmetic as written
 # (SURVEY.md §8(d)): d=1 25, d=2 148, d=3 478

@@ -42,7 +42,7 @@ cudaError_t launch_build_ev_slabs(double *hist, double *ev_hist, int d, int N, i
 }  // namespace nufi
 
 namespace nufi {
-cudaError_t launch_field_update(const FieldParams &p, cudaStream_t st);
+cudaError_t launch_field_update(const FieldParams &p, cudaStream_t st, int threads);
 cudaError_t launch_rho_bar(const RhoBarParams &p, cudaStream_t st);
 }  // namespace nufi
 
@@ -612,6 +612,9 @@ static TraceRhoParams trace_params(nufi_handle *h, int64_t n, int b_lo) {
     return p;
 }
 
+// CTA width of every d = 1 tail (see launch_field_update); 0 = by size for d >= 2
+static int field_threads(const nufi_handle *h) { return h->d == 1 ? h->threads + 32 : 0; }
+
 static FieldParams field_params(nufi_handle *h) {
     FieldParams f{};
     f.d = h->d;
@@ -703,7 +706,7 @@ static int enqueue_step(nufi_handle *h, int64_t n, bool full, const StepOut &o) 
     f.minmax = h->blocks + (size_t)h->B * h->nodes;
     f.mm_per_block = 1;
     ProfScope ps(h, 2);
-    CU(launch_field_update(f, h->stream));
+    CU(launch_field_update(f, h->stream, field_threads(h)));
     return NUFI_OK;
 }
 
@@ -770,7 +773,7 @@ int nufi_rho_finish(nufi_handle *h, const double *partials, double *rho_out, dou
     f.finish_only = 1;
     {
         ProfScope ps(h, 2);
-        CU(launch_field_update(f, h->stream));
+        CU(launch_field_update(f, h->stream, field_threads(h)));
     }
     return copy_step_outputs(h, rho_out, nullptr, nullptr, stats3);
 }
@@ -800,7 +803,7 @@ int nufi_field_update(nufi_handle *h, const double *rho, double *W_out, double *
     f.E_out = h->d_E;
     {
         ProfScope ps(h, 2);
-        CU(launch_field_update(f, h->stream));
+        CU(launch_field_update(f, h->stream, field_threads(h)));
     }
     int rc = check_status(h, "solve_poisson");
     if (rc) return rc;
@@ -851,7 +854,7 @@ int nufi_step_finish(nufi_handle *h, int64_t n, const double *partials, double *
     f.E_out = h->d_E;
     {
         ProfScope ps(h, 2);
-        CU(launch_field_update(f, h->stream));
+        CU(launch_field_update(f, h->stream, field_threads(h)));
     }
     int rc = check_status(h, "solve_poisson");
     if (rc) return rc;
@@ -880,7 +883,7 @@ int nufi_step_finish_async(nufi_handle *h, int64_t n, const double *partials, do
     f.E_out = E_out;
     {
         ProfScope ps(h, 2);
-        CU(launch_field_update(f, h->stream));
+        CU(launch_field_update(f, h->stream, field_threads(h)));
     }
     h->len += 1;  // provisional; nufi_check_status() reconciles with the device length
     return NUFI_OK;

@@ -528,8 +528,9 @@ static __device__ __forceinline__ bool field_update_body(const FieldParams &p, d
     }
 
     NUFI_STAMP(p, 3);
+    // lanes per DFT output from the grid alone (not the CTA width): fixed summation order
     int G = 1;
-    while (G < 32 && 2 * G <= N && (long long)nodes * 2 * G <= T) G *= 2;
+    while (G < 32 && 2 * G <= N && (long long)nodes * 2 * G <= 256) G *= 2;
 
     // ---- forward DFT (poisson.py:77) ----
     double *ar = re0, *ai = im0, *br = re1, *bi = im1;

@@ -23,11 +23,15 @@ size_t field_update_smem_bytes(int d, int nodes, int N) {
     return (size_t)field_smem_doubles(nodes, N, d == 1) * sizeof(double);
 }
 
-cudaError_t launch_field_update(const FieldParams &p, cudaStream_t st) {
+// threads: 0 = by size; d = 1 handles pass their trace-kernel CTA width so every d = 1
+// tail (persistent run kernel, fused step kernel, this kernel) runs with the same
+// block size -- the CTA-wide reductions then group identically and the results of
+// nufi_run, nufi_step and the multi-rank path are bit-identical.
+cudaError_t launch_field_update(const FieldParams &p, cudaStream_t st, int threads_req) {
     const size_t smem = field_update_smem_bytes(p.d, p.nodes, p.N);
     cudaError_t e = cudaFuncSetAttribute(field_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const int threads = p.nodes >= 1024 ? 1024 : (p.nodes >= 128 ? 512 : 256);
+    const int threads = threads_req > 0 ? threads_req : (p.nodes >= 1024 ? 1024 : (p.nodes >= 128 ? 512 : 256));
     field_update_kernel<<<1, threads, smem, st>>>(p);
     return cudaGetLastError();
 }

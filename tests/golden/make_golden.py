@@ -52,6 +52,10 @@ CONFIGS = {
     "tiny2": dict(d=2, Nx=8, Nv=8, vmax=6.0, tau=1 / 8, N=24, bench="strong_landau_2d", alpha=0.5, keep=25),
     "tiny3": dict(d=3, Nx=8, Nv=4, vmax=6.0, tau=1 / 8, N=12, bench="two_stream_3d", alpha=None, keep=13),
     "eq1": dict(d=1, Nx=32, Nv=128, vmax=10.0, tau=1 / 16, N=160, bench="weak_landau_1d", alpha=0.0, keep=1),
+    # ragged / non-power-of-two grids (generic-N kernel paths, Nv^d not a multiple of 32 or 8)
+    "rag1": dict(d=1, Nx=24, Nv=40, vmax=6.0, tau=1 / 8, N=40, bench="weak_landau_1d", alpha=0.05, keep=41),
+    "rag2": dict(d=2, Nx=6, Nv=10, vmax=6.0, tau=1 / 8, N=16, bench="strong_landau_2d", alpha=0.3, keep=17),
+    "rag3": dict(d=3, Nx=5, Nv=3, vmax=5.0, tau=1 / 8, N=8, bench="weak_landau_3d", alpha=0.05, keep=9),
     # FP32 history mode (PotentialHistory(dtype=float32), spline.py:118-125)
     "kat_wl_f32": dict(d=1, Nx=32, Nv=128, vmax=10.0, tau=1 / 16, N=160, bench="weak_landau_1d", alpha=None,
                        keep=161, dtype="float32"),
@@ -61,7 +65,7 @@ CONFIGS = {
 
 
 # history length used for the trace goldens
-TRACE_N = {"kat_wl": 40, "tiny2": 20, "tiny3": 12, "wl3r": 16}
+TRACE_N = {"kat_wl": 40, "tiny2": 20, "tiny3": 12, "wl3r": 16, "rag1": 30, "rag2": 12, "rag3": 7}
 
 
 def build(cfg):
@@ -178,7 +182,8 @@ def trace_goldens(name, g, stack, tau, n, M=2000, seed=1234):
 
 
 # steps at which the observable sweep goldens are taken (Psi needs fields 0..n)
-SWEEP_N = {"kat_wl": (0, 1, 20, 40), "tiny2": (0, 3, 10, 20), "tiny3": (0, 2, 6, 11), "wl3r": (0, 5, 16)}
+SWEEP_N = {"kat_wl": (0, 1, 20, 40), "tiny2": (0, 3, 10, 20), "tiny3": (0, 2, 6, 11), "wl3r": (0, 5, 16),
+           "rag1": (0, 7, 30), "rag2": (0, 5, 15), "rag3": (0, 3, 7)}
 
 
 def conserved_weights():

@@ -63,7 +63,7 @@ def _ctx(name, rows):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["kat_wl", "tiny2", "tiny3", "wl3r"])
+@pytest.mark.parametrize("name", ["kat_wl", "tiny2", "tiny3", "wl3r", "rag1", "rag2", "rag3"])
 def test_conserved_moments_vs_reference(name):
     z = golden(f"sweep_{name}")
     steps = [int(n) for n in z["steps"]]

@@ -65,7 +65,7 @@ def sharded_run(name, N, world, B=8, asynchronous=False):
     return rho, W, hists, evals
 
 
-@pytest.mark.parametrize("name,N", [("kat_wl", 40), ("tiny2", 12), ("tiny3", 8)])
+@pytest.mark.parametrize("name,N", [("kat_wl", 40), ("tiny2", 12), ("tiny3", 8), ("rag1", 20)])
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_sharded_bit_identical_to_single_gpu(name, N, world):
     w = workload(name)

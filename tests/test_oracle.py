@@ -15,8 +15,8 @@ import pytest
 from oracle import oracle as O
 from tests._util import golden, normwise
 
-TRACE_CASES = ["kat_wl", "tiny2", "tiny3", "wl3r"]
-LOOP_CASES = ["kat_wl", "eq1", "tiny2", "tiny3", "wl1", "kat_wl_f32", "tiny2_f32"]
+TRACE_CASES = ["kat_wl", "tiny2", "tiny3", "wl3r", "rag1", "rag2", "rag3"]
+LOOP_CASES = ["kat_wl", "eq1", "tiny2", "tiny3", "wl1", "kat_wl_f32", "tiny2_f32", "rag1", "rag2", "rag3"]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -117,7 +117,7 @@ def test_kat_equilibrium():
     assert np.all(golden("eq1")["W"] < 1e-20)
 
 
-@pytest.mark.parametrize("name", ["kat_wl", "tiny2", "tiny3", "wl3r"])
+@pytest.mark.parametrize("name", ["kat_wl", "tiny2", "tiny3", "wl3r", "rag1", "rag2", "rag3"])
 def test_sweep_vs_reference(name):
     """Oracle quadrature_sweep_many (Psi) vs the reference's, conserved-quantity weights."""
     z = golden(f"sweep_{name}")
