@@ -284,10 +284,18 @@ static void choose_tiling(nufi_handle *h) {
         if (const char *e = getenv("NUFI_PASSES")) passes = std::max(1, atoi(e));
     }
     while (warps > 1 && (per_block % (warps * ppt) != 0)) warps >>= 1;
+    if (h->d == 1) {
+        // latency-bound small grids: fewer rows per tile so the tiles spread over all SMs
+        // (wl1: 64 tiles of 8 rows -> 128 tiles of 4); the CTA stays 9 warps wide
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+        const int64_t nt = (h->nodes + 31) / 32;
+        while (warps > 1 && (h->V / (warps / 2)) * nt <= sms && per_block % (warps / 2) == 0) warps >>= 1;
+    }
     while (ppt > 1 && (per_block % (warps * ppt) != 0)) ppt >>= 1;
     while (passes > 1 && (per_block % ((int64_t)warps * ppt * passes) != 0)) passes >>= 1;
     if (per_block % ((int64_t)warps * ppt * passes) != 0) warps = ppt = passes = 1;
-    h->threads = warps * 32;
+    h->threads = h->d == 1 ? 256 : warps * 32;  // d = 1: 8 warp slots (+ producer), `warps` of them trace
     h->ppt = ppt;
     h->passes = passes;
     h->vt_rows = warps * ppt * passes;
@@ -1100,7 +1108,8 @@ int nufi_moments(nufi_handle *h, int64_t n, double *out, int64_t *evals) {
     const int nm = mom_sums(h->d) + 2;
     const int ctas = (h->b_hi - h->b_lo) * h->vt_per_block * h->node_tiles;
     if (!h->mom_part) {
-        CU(dalloc(&h->mom_part, (size_t)h->vt_total * h->node_tiles * nm * sizeof(double), h->stream));
+        const size_t rows = h->d == 1 ? (size_t)h->V : (size_t)h->vt_total;  // d = 1 sweep tiles may be finer
+        CU(dalloc(&h->mom_part, rows * h->node_tiles * nm * sizeof(double), h->stream));
         CU(dalloc(&h->d_mom, 16 * sizeof(double), h->stream));
     }
     TraceRhoParams p = trace_params(h, n, h->b_lo);
@@ -1109,12 +1118,26 @@ int nufi_moments(nufi_handle *h, int64_t n, double *out, int64_t *evals) {
     // spill the 2-point d = 3 variant); the same rows in twice the passes
     const int ppt = 1;
     p.passes = h->passes * h->ppt;
+    int threads = h->threads, ctas_s = ctas;
+    if (h->d == 1) {
+        // its own tiles: w rows strided across each residue-class block (d1_row), so a
+        // rank's share of blocks is exactly its share of rows
+        const int rpb = (int)(h->V / h->B);
+        int w = 8;
+        while (w > 1 && rpb % w) w >>= 1;
+        p.vt_rows = w;
+        p.passes = 1;
+        p.vt_per_block = rpb / w;
+        p.vt_lo = h->b_lo * p.vt_per_block;
+        threads = 32 * w;
+        ctas_s = (h->b_hi - h->b_lo) * p.vt_per_block * h->node_tiles;
+    }
     const double measure = std::pow(h->hx, (double)h->d) * h->hv_d;  // density.py:107
     {
         ProfScope ps(h, 0, point_steps(h, n > 0 ? n + 1 : 0, h->b_hi - h->b_lo));
-        CU(launch_sweep_moments(h->d, ppt, h->pow2, p, h->K, ctas, h->threads, h->stream));
+        CU(launch_sweep_moments(h->d, ppt, h->pow2, p, h->K, ctas_s, threads, h->stream));
     }
-    CU(launch_reduce_moments(h->mom_part, ctas, h->d, measure, h->d_mom, h->stream));
+    CU(launch_reduce_moments(h->mom_part, ctas_s, h->d, measure, h->d_mom, h->stream));
     CU(cudaMemcpyAsync(out, h->d_mom, nm * sizeof(double), cudaMemcpyDefault, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     if (evals && n > 0) *evals += (int64_t)point_steps(h, n + 1, h->b_hi - h->b_lo);

@@ -71,9 +71,11 @@ template <int NX, int SPS>
 __global__ void __launch_bounds__(288, 2) run_1d_kernel(const Run1DParams P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const TraceRhoParams &p = P.tp;
-    const int cw = (blockDim.x >> 5) - 1;  // consumer warps; the last warp is the TMA producer
+    // warps [0, cw) trace (cw = tile rows), the last warp is the TMA producer, any
+    // warps in between only help with the tail (the CTA is 9 warps wide for it)
+    const int cw = p.vt_rows;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const bool producer = warp == cw;
+    const bool producer = warp == (int)(blockDim.x >> 5) - 1;
     const int N = NX ? NX : p.N;
     const int SLAB = NX ? ev_slab_elems(1, NX) : p.ev_slab_elems;
     const int stages = p.stages;
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(288, 2) run_1d_kernel(const Run1DParams P) {
                         if (++s_ring == stages) s_ring = 0, ph_ring ^= 1u;
                     }
                 }
-            } else {
+            } else if (warp < cw) {
                 const bool valid = node < nodes;
                 const int j = d1_row(vt, warp, p.vt_per_block, p.B);
                 const double v0 = __dadd_rn(-p.vmax, __dmul_rn((double)j + 0.5, p.hv));  // grids.py:110-115

@@ -99,7 +99,8 @@ __global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams 
         int64_t jrow[PPT];
 #pragma unroll
         for (int pp = 0; pp < PPT; ++pp) {
-            jrow[pp] = (int64_t)vt * p.vt_rows + (int64_t)(pass * warps + warp) * PPT + pp;
+            jrow[pp] = D == 1 ? (int64_t)d1_row(vt, (pass * warps + warp) * PPT + pp, p.vt_per_block, p.B)
+                              : (int64_t)vt * p.vt_rows + (int64_t)(pass * warps + warp) * PPT + pp;
             int64_t r = jrow[pp];
 #pragma unroll
             for (int a = D - 1; a >= 0; --a) {

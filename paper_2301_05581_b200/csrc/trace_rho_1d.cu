@@ -57,9 +57,9 @@ template <int NX, int SPS>
 __global__ void __launch_bounds__(288) trace_rho_1d_kernel(const TraceRhoParams p, const FieldParams fp, int fuse,
                                                             unsigned *ticket) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int cw = (blockDim.x >> 5) - 1;  // consumer warps
+    const int cw = p.vt_rows;  // tracing warps (tile rows); the last warp is the producer
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const bool producer = warp == cw;
+    const bool producer = warp == (int)(blockDim.x >> 5) - 1;
     const int N = NX ? NX : p.N;
     const int SLAB = NX ? ev_slab_elems(1, NX) : p.ev_slab_elems;
     const int stages = p.stages;
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(288) trace_rho_1d_kernel(const TraceRhoParams 
     const int tile = blockIdx.x % p.node_tiles;
     const int vt = p.vt_lo + blockIdx.x / p.node_tiles;
     const int node = tile * 32 + lane;
-    const bool valid = node < p.nodes && !producer;
+    const bool valid = node < p.nodes && !producer && warp < cw;
     const int n = p.n;
     const int groups = (n + SPS - 1) / SPS;  // slab groups g = k / SPS, consumed g_top .. 0
 
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(288) trace_rho_1d_kernel(const TraceRhoParams 
                 if (++s == stages) s = 0, ph ^= 1u;
             }
         }
-    } else {
+    } else if (warp < cw) {
         // point (x_i, v_j): grids.py:104-115
         const int j = d1_row(vt, warp, p.vt_per_block, p.B);
         const double v0 = __dadd_rn(-p.vmax, __dmul_rn((double)j + 0.5, p.hv));

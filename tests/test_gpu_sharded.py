@@ -88,3 +88,34 @@ def test_sharded_async_finish_bit_identical(name, N):
     for r in range(2):
         assert np.array_equal(rho[r], ref.rho) and np.array_equal(W[r], ref.W)
 
+
+
+@pytest.mark.parametrize("name,N", [("kat_wl", 30), ("tiny3", 6)])
+def test_distributed_simulation_nccl_single_rank(name, N):
+    """The real torch.distributed / NCCL plumbing of dist.DistributedSimulation with one
+    rank (no other rank to wait for): async device-output loop, bit-identical to one GPU."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2301_05581_b200.dist import DistributedSimulation
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        w = workload(name)
+        g = w.grid
+        ds = DistributedSimulation(g, w.ic, w.tau, N)
+        out = dict(rho=torch.empty((N + 1, g.n_nodes), dtype=torch.float64, device="cuda"),
+                   W=torch.empty(N + 1, dtype=torch.float64, device="cuda"))
+        ds.run(outputs=out)
+        torch.cuda.synchronize()
+        ref = nufi.Simulation(g, w.ic, w.tau, N, v_blocks=ds.B).run()
+        assert np.array_equal(out["rho"].cpu().numpy(), ref.rho)
+        assert np.array_equal(out["W"].cpu().numpy(), ref.W)
+        assert len(ds.history) == N + 1
+    finally:
+        dist.destroy_process_group()
