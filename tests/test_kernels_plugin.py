@@ -1,0 +1,62 @@
+"""paper_2301_05581_b200.kernels: the reference's trace plug-in point (kernels.py:30-45,
+390-412) served by the GPU -- same signature, in-place contract, evaluation count and
+errors; the default backend is bit-identical to the reference's numba kernels."""
+
+import numpy as np
+import pytest
+
+from paper_2301_05581_b200 import kernels as K
+from paper_2301_05581_b200.errors import UsageError
+from tests._util import golden
+
+CASES = ["kat_wl", "tiny2", "tiny3", "wl3r", "rag1", "rag2", "rag3"]
+
+
+def _stack(t, rows):
+    n = int(t["n"])
+    c = t["coeffs"][:rows]
+    N = round(c.shape[1] ** (1.0 / t["Xin"].shape[1]))
+    return c.reshape((rows,) + (N,) * t["Xin"].shape[1]), n
+
+
+def test_contract_without_gpu():
+    X = np.zeros((4, 1))
+    V = np.zeros((4, 1))
+    c = np.zeros((3, 8))
+    assert K.trace_backward(c, 1.0, 0, 0.1, X, V, True) == 0  # n = 0: no-op (kernels.py:397)
+    assert K.trace_backward(c, 1.0, 2, 0.1, X[:0], V[:0], False) == 0  # M = 0
+    with pytest.raises(UsageError):
+        K.trace_backward(c, 1.0, 3, 0.1, X, V, True)  # needs 4 fields
+    with pytest.raises(UsageError):
+        K.set_backend("numba")
+    assert K.get_backend() in ("b200-parity", "b200")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("hk", [0, 1])
+def test_plugin_bit_exact_vs_numba(name, hk):
+    t = golden(f"trace_{name}")
+    n = int(t["n"])
+    stack, _ = _stack(t, n + 1)
+    X, V = t["Xin"].copy(), t["Vin"].copy()
+    K.set_backend("b200-parity")
+    ev = K.trace_backward(stack, float(t["L"]), n, float(t["tau"]), X, V, bool(hk))
+    assert ev == int(t[f"evals{hk}"])
+    assert np.array_equal(X, t[f"X{hk}"]) and np.array_equal(V, t[f"V{hk}"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["kat_wl", "tiny3"])
+def test_plugin_fast_backend_close(name):
+    t = golden(f"trace_{name}")
+    n = int(t["n"])
+    stack, _ = _stack(t, n + 1)
+    X, V = t["Xin"].copy(), t["Vin"].copy()
+    K.set_backend("b200")
+    try:
+        K.trace_backward(stack, float(t["L"]), n, float(t["tau"]), X, V, True)
+    finally:
+        K.set_backend("b200-parity")
+    scale = max(np.abs(t["X1"]).max(), np.abs(t["V1"]).max())
+    assert np.abs(X - t["X1"]).max() <= 1e-11 * scale and np.abs(V - t["V1"]).max() <= 1e-11 * scale
