@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--impl", default="nufi", choices=["nufi", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU sample length")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="test hook: take the multi-rank (NCCL) code path even with one rank")
     return ap.parse_args()
 
 
@@ -186,6 +188,7 @@ def flush_l2(torch, buf):
 
 
 def gpu_arm(args, rank: int, world: int):
+    dist_mode = world > 1 or args.force_dist
     import ctypes
 
     import torch
@@ -204,7 +207,7 @@ def gpu_arm(args, rank: int, world: int):
     flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")
     stream = torch.cuda.current_stream()
 
-    if world > 1:
+    if dist_mode:
         import torch.distributed as dist
 
         from paper_2301_05581_b200.dist import DistributedSimulation
@@ -222,7 +225,7 @@ def gpu_arm(args, rank: int, world: int):
         sim.run(outputs=dev_out)
 
     def barrier():
-        if world > 1:
+        if dist_mode:
             torch.distributed.barrier()
 
     for _ in range(args.warmup):
@@ -248,7 +251,7 @@ def gpu_arm(args, rank: int, world: int):
             wall.append(time.perf_counter() - t0)
             times.append(e0.elapsed_time(e1) / 1e3)
     t_dev = float(np.sum(times))
-    if world > 1:
+    if dist_mode:
         tt = torch.tensor([t_dev], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_dev = float(tt.item())
@@ -259,7 +262,7 @@ def gpu_arm(args, rank: int, world: int):
     # ---- e2e: the public API with host outputs (per-step D2H inside the timed region) ----
     e2e_times = []
     d2h = steps_per_run * (g.n_nodes * (1 + g.d) + 4) * 8
-    if world == 1:
+    if not dist_mode:
         for i in range(args.warmup + args.steps):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
@@ -269,7 +272,20 @@ def gpu_arm(args, rank: int, world: int):
                 e2e_times.append(time.perf_counter() - t0)
         e2e_value = args.steps * ps_run / float(np.sum(e2e_times))
     else:
-        e2e_value = None
+        # every rank: DistributedSimulation(...).run() -> host arrays; max over ranks
+        from paper_2301_05581_b200.dist import DistributedSimulation
+
+        for i in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            torch.distributed.barrier()
+            t0 = time.perf_counter()
+            res = DistributedSimulation(g, w.ic, w.tau, N).run()
+            _ = float(res["W"][-1])
+            t_run = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+            torch.distributed.all_reduce(t_run, op=torch.distributed.ReduceOp.MAX)
+            if i >= args.warmup:
+                e2e_times.append(float(t_run.item()))
+        e2e_value = args.steps * ps_run / float(np.sum(e2e_times))
 
     # ---- roofline: one additional identical run with per-launch CUDA events ----
     h = sim.history.handle
@@ -317,11 +333,13 @@ def gpu_arm(args, rank: int, world: int):
             "data": "synthetic (deterministic BASELINE config; no dataset)",
             "config": {"workload": args.config, "description": w.description, "time_steps_per_run": steps_per_run,
                        "point_steps_per_run": ps_run, "l2": "flushed (256 MiB write) between timed runs",
-                       "parallelism": f"v-block sharding x{world}" if world > 1 else "single GPU"},
+                       "parallelism": f"v-block sharding x{world}" if dist_mode else "single GPU"},
             "wall_s_to_t_end": ms_per_run / 1e3,
             "e2e": {"value": e2e_value, "unit": "point-steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": d2h,
-                    "api": "Simulation(grid, ic, tau, N).run() -> host numpy rho/E/W/stats per time step"},
+                    "api": ("Simulation(grid, ic, tau, N).run()" if not dist_mode else
+                            "DistributedSimulation(grid, ic, tau, N).run() on every rank (max over ranks)")
+                           + " -> host numpy rho/E/W/stats per time step"},
             "gpu_launches": launches_per_run * args.steps,
             "roofline": roofline,
             "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
@@ -337,14 +355,19 @@ def main():
     if args.impl == "reference":
         reference_arm(args, rank)
         return
-    if world > 1:
+    dist_mode = world > 1 or args.force_dist
+    if dist_mode:
         import torch
         import torch.distributed as dist
 
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         dist.init_process_group("nccl")
     gpu_arm(args, rank, world)
-    if world > 1:
+    if dist_mode:
         import torch.distributed as dist
 
         dist.destroy_process_group()

@@ -124,13 +124,27 @@ class DistributedSimulation:
         return n
 
     def run(self, outputs: dict | None = None):
-        """The whole loop.  With device (CUDA tensor) outputs, or none, every step is
-        enqueued without a host synchronisation (trace -> NCCL allreduce -> field
-        update, all on one stream); the status is checked once at the end."""
+        """The whole loop.  With device (CUDA tensor) outputs every step is enqueued
+        without a host synchronisation (trace -> NCCL allreduce -> field update, all on
+        one stream) and the status is checked once at the end.  outputs=None: the same,
+        into internal device buffers, returning host numpy arrays (the public call,
+        like Simulation.run)."""
         first = len(self.history)
-        dev = all(v is None or hasattr(v, "data_ptr") for v in (outputs or {}).values())
+        steps = self.n_steps + 1 - first
+        host = outputs is None
+        if host:
+            g = self.grid
+            t = self.torch
+            dev = f"cuda:{self.partials.device.index}"
+            outputs = dict(rho=t.empty((steps, g.n_nodes), dtype=t.float64, device=dev),
+                           E=t.empty((steps, g.n_nodes, g.d), dtype=t.float64, device=dev),
+                           W=t.empty(steps, dtype=t.float64, device=dev),
+                           stats=t.empty((steps, 3), dtype=t.float64, device=dev))
+        on_device = all(v is None or hasattr(v, "data_ptr") for v in outputs.values())
         for n in range(first, self.n_steps + 1):
-            self.step(outputs, n - first, sync=not dev)
-        if dev:
+            self.step(outputs, n - first, sync=not on_device)
+        if on_device:
             self.history.handle.call("nufi_check_status")
+        if host:
+            return {k: v.cpu().numpy() for k, v in outputs.items()}
         return outputs

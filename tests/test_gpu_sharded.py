@@ -117,5 +117,7 @@ def test_distributed_simulation_nccl_single_rank(name, N):
         assert np.array_equal(out["rho"].cpu().numpy(), ref.rho)
         assert np.array_equal(out["W"].cpu().numpy(), ref.W)
         assert len(ds.history) == N + 1
+        host = DistributedSimulation(g, w.ic, w.tau, N).run()  # public call: host arrays
+        assert np.array_equal(host["rho"], ref.rho) and np.array_equal(host["W"], ref.W)
     finally:
         dist.destroy_process_group()
