@@ -189,6 +189,12 @@ int nufi_trace(nufi_handle *h, int64_t n, double *X, double *V, int64_t M, int h
  * out: 6 + d doubles.  evals (optional) += points * (n + 1) for n > 0. */
 int nufi_moments(nufi_handle *h, int64_t n, double *out, int64_t *evals);
 
+/* SplineField.eval_phi_many / eval_E_many (spline.py:46-52, kernels.py:84-123) of
+ * stored field `slot` at caller points X (M, d): phi_out (M) and E_out (M, d) = minus
+ * the spline gradient, each optional; host or device buffers.  The numpy twin's
+ * operation order, no FMA: bit-identical to the reference. */
+int nufi_eval_field(nufi_handle *h, int64_t slot, const double *X, int64_t M, double *phi_out, double *E_out);
+
 /* f0 at caller points (eval_f0, initial.py:165-180): F[M]. */
 int nufi_eval_f0(nufi_handle *h, const double *X, const double *V, int64_t M, double *F);
 

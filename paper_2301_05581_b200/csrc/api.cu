@@ -29,6 +29,8 @@ cudaError_t launch_reduce_blocks(const double *partial, const double *fminmax, d
 cudaError_t launch_trace_points(int d, int mode, bool pow2, const double *hist, const double *ev_hist,
                                 int ev_slab_elems, int N, int nodes, double L, int n, double tau, double K, double *X,
                                 double *V, int64_t M, int half_kick, cudaStream_t st);
+cudaError_t launch_eval_field(int d, const double *c, int N, double L, const double *X, int64_t M, double *phi,
+                              double *E, cudaStream_t st);
 cudaError_t launch_eval_f0(int d, const F0Params &f0, const double *X, const double *V, int64_t M, double *F,
                            cudaStream_t st);
 cudaError_t launch_trace_rho_1d(const TraceRhoParams &p, const FieldParams &fp, int fuse, unsigned *ticket, int ctas,
@@ -1141,6 +1143,36 @@ int nufi_moments(nufi_handle *h, int64_t n, double *out, int64_t *evals) {
     CU(cudaMemcpyAsync(out, h->d_mom, nm * sizeof(double), cudaMemcpyDefault, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     if (evals && n > 0) *evals += (int64_t)point_steps(h, n + 1, h->b_hi - h->b_lo);
+    return NUFI_OK;
+}
+
+int nufi_eval_field(nufi_handle *h, int64_t slot, const double *X, int64_t M, double *phi_out, double *E_out) {
+    CHECK_HANDLE(h);
+    if (slot < 0 || slot >= h->len) return fail(NUFI_ERR_USAGE, "history has no entry at that index");  // spline.py:144-146
+    if (M == 0) return NUFI_OK;
+    if (!X) return fail(NUFI_ERR_USAGE, "null points");
+    const size_t bytes = (size_t)M * h->d * sizeof(double);
+    const double *dX = X;
+    double *tX = nullptr, *dphi = phi_out, *dE = E_out, *tphi = nullptr, *tE = nullptr;
+    if (!is_device_ptr(X)) {
+        CU(cudaMallocAsync(&tX, bytes, h->stream));
+        CU(cudaMemcpyAsync(tX, X, bytes, cudaMemcpyHostToDevice, h->stream));
+        dX = tX;
+    }
+    if (phi_out && !is_device_ptr(phi_out)) {
+        CU(cudaMallocAsync(&tphi, (size_t)M * sizeof(double), h->stream));
+        dphi = tphi;
+    }
+    if (E_out && !is_device_ptr(E_out)) {
+        CU(cudaMallocAsync(&tE, bytes, h->stream));
+        dE = tE;
+    }
+    CU(launch_eval_field(h->d, h->hist + (size_t)slot * h->nodes, h->N, h->cfg.L, dX, M, dphi, dE, h->stream));
+    if (tphi) CU(cudaMemcpyAsync(phi_out, tphi, (size_t)M * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    if (tE) CU(cudaMemcpyAsync(E_out, tE, bytes, cudaMemcpyDeviceToHost, h->stream));
+    for (void *q : {(void *)tX, (void *)tphi, (void *)tE})
+        if (q) CU(cudaFreeAsync(q, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
     return NUFI_OK;
 }
 

@@ -165,9 +165,6 @@ __global__ void trace_points_parity(const double *__restrict__ hist, int N, int 
     }
 }
 
-#undef M_
-#undef A_
-#undef S_
 
 // Production arithmetic on caller points.  The optional leading half kick
 // (Psi, flow.py:106-112) uses slab n.
@@ -192,6 +189,75 @@ __global__ void trace_points_fast(const double *__restrict__ ev_hist, int ev_sla
         X[p * D + a] = (Xs[a] + 0.5) * hx;
         V[p * D + a] = Vs[a] * s_out;
     }
+}
+
+// SplineField.eval_phi_many / eval_E_many (spline.py:46-52 -> kernels.py:84-123, the numpy
+// twin): _locate (np.mod, u >= L -> 0), bspline_weights / dweights, the 4^d stencil in
+// itertools.product order (x tap slowest), phi += c * prod w, E_g -= c * prod (dw on axis
+// g, w elsewhere), E *= N / L; elementwise IEEE operations in numpy's order, no FMA.
+template <int D>
+__global__ void eval_field_kernel(const double *__restrict__ c, int N, double L, const double *__restrict__ X,
+                                  int64_t M, double *__restrict__ phi_out, double *__restrict__ E_out) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= M) return;
+    const double inv_h = (double)N / L;
+    int i[D];
+    double w[D][4], dw[D][4];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        double f;
+        cell_1d_exact(X[p * D + a], L, N, inv_h, i[a], f);
+        fill_weights_exact(f, w[a], dw[a]);
+    }
+    double phi = 0.0, E[D];
+#pragma unroll
+    for (int g = 0; g < D; ++g) E[g] = 0.0;
+    constexpr int TAPS = D == 1 ? 4 : (D == 2 ? 16 : 64);
+    for (int t = 0; t < TAPS; ++t) {
+        int o[D];
+        int r = t;
+#pragma unroll
+        for (int a = D - 1; a >= 0; --a) {
+            o[a] = r & 3;
+            r >>= 2;
+        }
+        int idx = 0;
+        double wp = 1.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            int j = i[a] + o[a] - 1;
+            j = j < 0 ? j + N : (j >= N ? j - N : j);
+            idx = a == 0 ? j : idx * N + j;
+            wp = a == 0 ? w[0][o[0]] : M_(wp, w[a][o[a]]);
+        }
+        const double cv = c[idx];
+        phi = A_(phi, M_(cv, wp));
+#pragma unroll
+        for (int g = 0; g < D; ++g) {
+            double v = cv;
+#pragma unroll
+            for (int a = 0; a < D; ++a) v = M_(v, a == g ? dw[a][o[a]] : w[a][o[a]]);
+            E[g] = S_(E[g], v);
+        }
+    }
+    if (phi_out) phi_out[p] = phi;
+    if (E_out)
+#pragma unroll
+        for (int g = 0; g < D; ++g) E_out[p * D + g] = M_(E[g], inv_h);
+}
+
+#undef M_
+#undef A_
+#undef S_
+
+cudaError_t launch_eval_field(int d, const double *c, int N, double L, const double *X, int64_t M, double *phi,
+                              double *E, cudaStream_t st) {
+    const int threads = 128;
+    const int ctas = (int)((M + threads - 1) / threads);
+    if (d == 1) eval_field_kernel<1><<<ctas, threads, 0, st>>>(c, N, L, X, M, phi, E);
+    if (d == 2) eval_field_kernel<2><<<ctas, threads, 0, st>>>(c, N, L, X, M, phi, E);
+    if (d == 3) eval_field_kernel<3><<<ctas, threads, 0, st>>>(c, N, L, X, M, phi, E);
+    return cudaGetLastError();
 }
 
 template <int D>

@@ -12,7 +12,7 @@ from __future__ import annotations
 
 import ctypes
 import struct
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -24,14 +24,60 @@ from .initial import InitialCondition, VelocityProfile
 
 @dataclass(frozen=True)
 class SplineField:
-    """One stored potential: coefficient slab of shape grid.shape_x (spline.py:28-52)."""
+    """One stored potential: coefficient slab of shape grid.shape_x (spline.py:28-52).
+
+    eval_phi_many / eval_E_many run on the GPU (nufi_eval_field, the numpy twin's
+    operation order: bit-identical to the reference).  An entry of a device history
+    evaluates in place; a free-standing field is uploaded into a cached 1-slab history."""
 
     grid: GridSpec
     coeffs: np.ndarray
+    _source: tuple | None = field(default=None, compare=False, repr=False)  # (PotentialHistory, slot)
 
     @property
     def d(self) -> int:
         return self.grid.d
+
+    def nodal_values(self) -> np.ndarray:
+        """Potential values at the grid nodes (exact B-spline filter, spline.py:38-44)."""
+        phi = np.asarray(self.coeffs, dtype=np.float64)
+        for axis in range(self.grid.d):
+            phi = (np.roll(phi, 1, axis=axis) + 4.0 * phi + np.roll(phi, -1, axis=axis)) / 6.0
+        return phi
+
+    def _eval(self, X, want_phi: bool):
+        X = np.ascontiguousarray(np.atleast_2d(np.asarray(X, dtype=np.float64)))
+        if X.shape[1] != self.grid.d:
+            raise UsageError(f"position must have {self.grid.d} components")
+        if self._source is not None:
+            hist, slot = self._source
+        else:
+            hist, slot = _scratch_history(self.grid), 0
+            hist.load_stack(np.asarray(self.coeffs, dtype=np.float64).reshape((1,) + self.grid.shape_x))
+        M = X.shape[0]
+        out = np.empty(M) if want_phi else np.empty((M, self.grid.d))
+        hist.handle.call("nufi_eval_field", int(slot), X.ctypes.data, int(M),
+                         out.ctypes.data if want_phi else None, None if want_phi else out.ctypes.data)
+        return out
+
+    def eval_phi_many(self, X) -> np.ndarray:
+        """Spline values at X (M, d) (spline.py:46-48)."""
+        return self._eval(X, True)
+
+    def eval_E_many(self, X) -> np.ndarray:
+        """Minus the spline gradient at X (M, d) (spline.py:50-52)."""
+        return self._eval(X, False)
+
+
+_scratch: dict = {}
+
+
+def _scratch_history(grid: GridSpec) -> "PotentialHistory":
+    h = _scratch.get(grid)
+    if h is None:
+        h = PotentialHistory(grid, 1.0, capacity=1)
+        _scratch[grid] = h
+    return h
 
 
 def _current_device() -> int:
@@ -138,7 +184,7 @@ class PotentialHistory:
         self._handle.call("nufi_get_history", out.ctypes.data, int(m), 1)
         out = out.reshape(self.grid.shape_x).astype(self.dtype, copy=False)
         out.flags.writeable = False
-        return SplineField(grid=self.grid, coeffs=out)
+        return SplineField(grid=self.grid, coeffs=out, _source=(self, m))
 
     def stacked(self) -> np.ndarray:
         """Host copy (len, Nx, ..., Nx) of all stored coefficients (spline.py:151-155)."""

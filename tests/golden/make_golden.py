@@ -240,6 +240,30 @@ def checkpoint_goldens():
         hist.save(os.path.join(OUT, f"{base}_{rows}.vphist"))
 
 
+FIELD_SLOT = {"kat_wl": 20, "tiny2": 10, "tiny3": 6, "rag1": 12, "rag2": 8, "rag3": 5}
+
+
+def field_goldens():
+    """SplineField.eval_phi_many / eval_E_many (spline.py:46-52 -> kernels.py:84-123) of one
+    stored slab at seeded points plus edge positions (0, L, -tiny, nodes, far images)."""
+    from vpflow import spline
+
+    for base, slot in FIELD_SLOT.items():
+        g, _ = build(CONFIGS[base])
+        z = np.load(os.path.join(OUT, f"{base}.npz"))
+        c = z["coeffs"][slot].reshape((g.Nx,) * g.d)
+        fld = spline.SplineField(grid=g, coeffs=c)
+        rng = np.random.default_rng(99)
+        X = rng.uniform(-3 * g.L, 4 * g.L, size=(600, g.d))
+        edge = np.array([0.0, g.L, -1e-300, -5e-17, g.L * (1 - 1e-16), g.L / g.Nx, 3 * g.L / g.Nx, -g.L, 7 * g.L])
+        E = np.stack([np.resize(edge, 60)] * g.d, axis=1)
+        for a in range(g.d):
+            E[:, a] = np.roll(E[:, a], a)
+        X = np.concatenate([X, E])
+        np.savez_compressed(os.path.join(OUT, f"field_{base}.npz"), X=X, slot=np.array(slot),
+                            phi=fld.eval_phi_many(X), E=fld.eval_E_many(X))
+
+
 def host_info():
     try:
         cpu = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
@@ -255,6 +279,9 @@ def main(argv):
     sys.path.insert(0, REF)
     names = argv or list(CONFIGS)
     for name in names:
+        if name == "fields":
+            field_goldens()
+            continue
         if name == "checkpoints":
             checkpoint_goldens()
             continue

@@ -60,3 +60,30 @@ def test_plugin_fast_backend_close(name):
         K.set_backend("b200-parity")
     scale = max(np.abs(t["X1"]).max(), np.abs(t["V1"]).max())
     assert np.abs(X - t["X1"]).max() <= 1e-11 * scale and np.abs(V - t["V1"]).max() <= 1e-11 * scale
+
+
+FIELD_CASES = ["kat_wl", "tiny2", "tiny3", "rag1", "rag2", "rag3"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", FIELD_CASES)
+def test_spline_field_eval_bit_exact(name):
+    """SplineField.eval_phi_many / eval_E_many on the GPU vs the reference (numpy twin,
+    kernels.py:84-123) at seeded points and edge positions (0, L, -tiny, nodes, images)."""
+    import paper_2301_05581_b200 as nufi
+    from paper_2301_05581_b200.configs import workload
+
+    z = golden(f"field_{name}")
+    base = golden(name)
+    w = workload(name)
+    slot = int(z["slot"])
+    c = base["coeffs"][slot].reshape(w.grid.shape_x)
+    free = nufi.SplineField(grid=w.grid, coeffs=c)  # uploaded into a scratch history
+    assert np.array_equal(free.eval_phi_many(z["X"]), z["phi"])
+    assert np.array_equal(free.eval_E_many(z["X"]), z["E"])
+    h = nufi.PotentialHistory(w.grid, w.tau, capacity=slot + 1)
+    h.load_stack(base["coeffs"][: slot + 1].reshape((slot + 1,) + w.grid.shape_x))
+    entry = h.entry(slot)  # evaluated in place on the device history
+    assert np.array_equal(entry.eval_E_many(z["X"]), z["E"])
+    with pytest.raises(UsageError):
+        entry.eval_E_many(np.zeros((3, w.grid.d + 1)))
