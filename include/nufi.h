@@ -158,6 +158,16 @@ int64_t nufi_partials_len(nufi_handle *h); /* v_blocks * (Nx^d + 2) */
 int nufi_field_update(nufi_handle *h, const double *rho, double *W_out, double *E_out,
                       double *coeffs_out);
 
+/* The tail's reference operations one by one (Nx^d doubles, host or device buffers):
+ * solve_poisson (poisson.py:90-112): phi nodal values, the phi spectrum
+ * fftn(rho)/N^d/k^2 (zero and Nyquist modes dropped; spec_re / spec_im optional) and the
+ * electric energy (poisson.py:115-120, optional); NUFI_ERR_NUMERICAL if |mean rho| >
+ * 1e-8 max|rho|.  fit_spline (spline.py:71-86): periodic cubic B-spline coefficients
+ * of nodal values.  Neither touches the history. */
+int nufi_solve_poisson(nufi_handle *h, const double *rho, double *phi_out, double *spec_re, double *spec_im,
+                       double *W_out);
+int nufi_fit_spline(nufi_handle *h, const double *phi, double *coeffs_out);
+
 /* One full step n (requires len == n): nufi_rho + nufi_field_update, all on
  * the device.  Outputs optional. */
 int nufi_step(nufi_handle *h, int64_t n, double *rho_out, double *E_out, double *W_out,

@@ -16,6 +16,7 @@ from .flow import (TRACE_FAST, TRACE_PARITY, FlowContext, eval_f, eval_f0, eval_
                    psi_tilde, psi_tilde_batch, trace_backward)
 from .grids import GridSpec, PhasePoint, v_mid, v_mid_matrix, x_node, x_node_matrix
 from .initial import BENCHMARK_DEFAULTS, InitialCondition, VelocityProfile, make_benchmark, weak_landau_3d
-from .spline import PotentialHistory, SplineField
+from .poisson import SpectralField, electric_energy, solve_poisson, wavenumber_squared
+from .spline import PotentialHistory, SplineField, fit_spline
 
 __version__ = "0.1.0"

@@ -31,6 +31,8 @@ cudaError_t launch_trace_points(int d, int mode, bool pow2, const double *hist, 
                                 double *V, int64_t M, int half_kick, cudaStream_t st);
 cudaError_t launch_eval_field(int d, const double *c, int N, double L, const double *X, int64_t M, double *phi,
                               double *E, cudaStream_t st);
+cudaError_t launch_poisson_fit(const FieldParams &p, int mode, const double *in, double *out, double *spec_re,
+                               double *spec_im, double *W, int *status, cudaStream_t st);
 cudaError_t launch_eval_f0(int d, const F0Params &f0, const double *X, const double *V, int64_t M, double *F,
                            cudaStream_t st);
 cudaError_t launch_trace_rho_1d(const TraceRhoParams &p, const FieldParams &fp, int fuse, unsigned *ticket, int ctas,
@@ -1174,6 +1176,46 @@ int nufi_eval_field(nufi_handle *h, int64_t slot, const double *X, int64_t M, do
         if (q) CU(cudaFreeAsync(q, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     return NUFI_OK;
+}
+
+// solve_poisson / fit_spline one by one (host or device buffers of Nx^d doubles)
+static int poisson_fit(nufi_handle *h, int mode, const double *in, double *out, double *spec_re, double *spec_im,
+                       double *W_out) {
+    CHECK_HANDLE(h);
+    if (!in || !out) return fail(NUFI_ERR_USAGE, "null argument");
+    const size_t bytes = (size_t)h->nodes * sizeof(double);
+    // device staging: in, out, spec re / im, W (one allocation)
+    double *buf = nullptr;
+    CU(cudaMallocAsync(&buf, 4 * bytes + 64, h->stream));
+    double *din = buf, *dout = buf + h->nodes, *dre = buf + 2 * h->nodes, *dim = buf + 3 * h->nodes,
+           *dW = buf + 4 * h->nodes;
+    CU(cudaMemcpyAsync(din, in, bytes, cudaMemcpyDefault, h->stream));
+    CU(cudaMemsetAsync(h->d_status, 0, sizeof(int), h->stream));
+    FieldParams f = field_params(h);
+    CU(launch_poisson_fit(f, mode, din, dout, dre, dim, dW, h->d_status, h->stream));
+    int st = 0;
+    CU(cudaMemcpyAsync(&st, h->d_status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDefault, h->stream));
+    if (spec_re) CU(cudaMemcpyAsync(spec_re, dre, bytes, cudaMemcpyDefault, h->stream));
+    if (spec_im) CU(cudaMemcpyAsync(spec_im, dim, bytes, cudaMemcpyDefault, h->stream));
+    if (W_out) CU(cudaMemcpyAsync(W_out, dW, sizeof(double), cudaMemcpyDefault, h->stream));
+    CU(cudaFreeAsync(buf, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    if (st == NUFI_ERR_NUMERICAL) {
+        CU(cudaMemsetAsync(h->d_status, 0, sizeof(int), h->stream));
+        return fail(NUFI_ERR_NUMERICAL, "density is not neutral: nodal mean exceeds 1e-8 max|rho|; "
+                                        "subtract the mean before solving");  // poisson.py:98-104
+    }
+    return NUFI_OK;
+}
+
+int nufi_solve_poisson(nufi_handle *h, const double *rho, double *phi_out, double *spec_re, double *spec_im,
+                       double *W_out) {
+    return poisson_fit(h, 0, rho, phi_out, spec_re, spec_im, W_out);
+}
+
+int nufi_fit_spline(nufi_handle *h, const double *phi, double *coeffs_out) {
+    return poisson_fit(h, 1, phi, coeffs_out, nullptr, nullptr, nullptr);
 }
 
 int nufi_eval_f0(nufi_handle *h, const double *X, const double *V, int64_t M, double *F) {

@@ -18,6 +18,94 @@ __global__ void __launch_bounds__(1024) field_update_kernel(const FieldParams p)
     field_update_body(p, fsm);
 }
 
+// The separate reference operations of the step tail, for callers that use them one by
+// one (a single CTA, separable smem DFTs as in field_update_body):
+//   mode 0  solve_poisson (poisson.py:90-112): neutrality check (status 2, no output),
+//           spec = fftn(rho) / N^d / k^2 with the zero and Nyquist modes dropped,
+//           phi = Re ifftn(spec * N^d); W = L^d / 2 sum k^2 |spec|^2 (poisson.py:115-120)
+//   mode 1  fit_spline (spline.py:71-86): coeffs = Re ifftn(fftn(phi) / prod sym)
+// in: Nx^d reals; out: Nx^d reals; spec_re / spec_im / W optional (mode 0).
+__global__ void __launch_bounds__(1024) poisson_fit_kernel(FieldParams p, int mode, const double *in, double *out,
+                                                           double *spec_re, double *spec_im, double *W_out,
+                                                           int *status) {
+    extern __shared__ __align__(16) double fsm[];
+    const int nodes = p.nodes, N = p.N, d = p.d, T = blockDim.x;
+    double *ar = fsm, *ai = ar + nodes, *br = ai + nodes, *bi = br + nodes;
+    double *twc = bi + nodes, *tws = twc + N, *scratch = tws + N;
+    const bool pow2 = (N & (N - 1)) == 0;
+    for (int m = threadIdx.x; m < N; m += T) {
+        twc[m] = p.twc[m];
+        tws[m] = p.tws[m];
+    }
+    double s = 0.0, mx = 0.0;
+    for (int i = threadIdx.x; i < nodes; i += T) {
+        const double v = in[i];
+        ar[i] = v;
+        ai[i] = 0.0;
+        s += v;
+        mx = fmax(mx, fabs(v));
+    }
+    if (mode == 0) {  // poisson.py:98-104
+        const double mean = cta_sum(s, scratch) / (double)nodes;
+        const double tol = 1e-8 * cta_max(mx, scratch);
+        if (fabs(mean) > tol) {
+            if (threadIdx.x == 0) *status = NUFI_ERR_NUMERICAL;
+            return;
+        }
+    }
+    __syncthreads();
+    int G = 1;
+    while (G < 32 && 2 * G <= N && (long long)nodes * 2 * G <= 256) G *= 2;
+    for (int axis = d - 1; axis >= 0; --axis) {
+        int st = 1;
+        for (int a = axis + 1; a < d; ++a) st *= N;
+        dft_pass(ar, ai, br, bi, twc, tws, N, nodes, st, -1.0, G, pow2);
+        double *tr = ar, *ti = ai;
+        ar = br, ai = bi, br = tr, bi = ti;
+    }
+    double wsum = 0.0;
+    for (int e = threadIdx.x; e < nodes; e += T) {
+        const double sym = p.fac[nodes + e];
+        double f;
+        if (mode == 0) {
+            f = p.fac[e] * sym;  // 1 / (N^d k^2), 0 at the zero / Nyquist modes
+        } else {
+            f = 1.0 / ((double)nodes * sym);
+        }
+        const double pr = ar[e] * f, pi = ai[e] * f;
+        ar[e] = pr;
+        ai[e] = pi;
+        if (mode == 0) {
+            if (spec_re) spec_re[e] = pr;
+            if (spec_im) spec_im[e] = pi;
+            wsum += p.k2[e] * (pr * pr + pi * pi);
+        }
+    }
+    if (mode == 0) {
+        const double W = 0.5 * p.L_d * cta_sum(wsum, scratch);
+        if (W_out && threadIdx.x == 0) *W_out = W;
+    }
+    __syncthreads();
+    for (int axis = d - 1; axis >= 0; --axis) {
+        int st = 1;
+        for (int a = axis + 1; a < d; ++a) st *= N;
+        dft_pass(ar, ai, br, bi, twc, tws, N, nodes, st, 1.0, G, pow2);
+        double *tr = ar, *ti = ai;
+        ar = br, ai = bi, br = tr, bi = ti;
+    }
+    for (int i = threadIdx.x; i < nodes; i += T) out[i] = ar[i];
+}
+
+cudaError_t launch_poisson_fit(const FieldParams &p, int mode, const double *in, double *out, double *spec_re,
+                               double *spec_im, double *W, int *status, cudaStream_t st) {
+    const size_t smem = (4 * (size_t)p.nodes + 2 * p.N + 64) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(poisson_fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int threads = p.nodes >= 1024 ? 1024 : (p.nodes >= 128 ? 512 : 256);
+    poisson_fit_kernel<<<1, threads, smem, st>>>(p, mode, in, out, spec_re, spec_im, W, status);
+    return cudaGetLastError();
+}
+
 // d = 1 (field_update_1d_body) stages up to 8 block-sum rows; d = 2, 3 read the block table directly
 size_t field_update_smem_bytes(int d, int nodes, int N) {
     return (size_t)field_smem_doubles(nodes, N, d == 1) * sizeof(double);

@@ -69,6 +69,20 @@ class SplineField:
         return self._eval(X, False)
 
 
+def fit_spline(phi_nodes, grid: GridSpec, dtype=np.float64) -> SplineField:
+    """Interpolating periodic cubic spline through nodal values (spline.py:71-86), on the GPU."""
+    if grid.Nx < 4:
+        raise UsageError(f"spline fitting needs Nx >= 4, got {grid.Nx}")
+    phi = np.ascontiguousarray(np.asarray(phi_nodes, dtype=np.float64))
+    if phi.shape != grid.shape_x:
+        raise UsageError(f"phi_nodes must have shape {grid.shape_x}, got {phi.shape}")
+    out = np.empty(grid.n_nodes)
+    _scratch_history(grid).handle.call("nufi_fit_spline", phi.ctypes.data, out.ctypes.data)
+    coeffs = out.reshape(grid.shape_x).astype(dtype)
+    coeffs.flags.writeable = False
+    return SplineField(grid=grid, coeffs=coeffs)
+
+
 _scratch: dict = {}
 
 

@@ -87,3 +87,43 @@ def test_spline_field_eval_bit_exact(name):
     assert np.array_equal(entry.eval_E_many(z["X"]), z["E"])
     with pytest.raises(UsageError):
         entry.eval_E_many(np.zeros((3, w.grid.d + 1)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["kat_wl", "tiny2", "tiny3", "rag1", "rag2", "rag3", "wl3"])
+def test_solve_poisson_fit_spline_vs_reference(name):
+    """poisson.solve_poisson + spline.fit_spline + electric_energy one by one on the GPU vs
+    the reference's outputs (golden coefficients / W) and the pinned oracle (phi, spectrum)."""
+    import paper_2301_05581_b200 as nufi
+    from oracle import oracle as O
+    from paper_2301_05581_b200.configs import workload
+    from tests._util import normwise
+
+    g = golden(name)
+    w = workload(name)
+    for n in (0, 1, min(5, g["rho"].shape[0] - 1)):
+        rho = nufi.DensityGrid(w.grid, g["rho"][n].reshape(w.grid.shape_x))
+        phi, spec = nufi.solve_poisson(rho)
+        phi_o, hat_o = O.solve_poisson(O.case(name), g["rho"][n])
+        assert normwise(phi.reshape(1, -1), np.asarray(phi_o).reshape(1, -1))[0] <= 1e-12
+        assert np.abs(spec.coeffs.reshape(-1) - np.asarray(hat_o).reshape(-1)).max() <= 1e-12 * np.abs(hat_o).max()
+        assert abs(nufi.electric_energy(spec) / g["W"][n] - 1) <= 1e-12
+        fit = nufi.fit_spline(phi, w.grid)
+        assert normwise(np.asarray(fit.coeffs).reshape(1, -1), g["coeffs"][n: n + 1])[0] <= 1e-10
+    with pytest.raises(nufi.NumericalConsistencyError):
+        nufi.solve_poisson(nufi.DensityGrid(w.grid, np.full(w.grid.shape_x, 0.3)))
+
+
+@pytest.mark.gpu
+def test_poisson_eigenfunction_kat():
+    """rho = cos(2 pi x / L) -> phi = (L / 2 pi)^2 cos(2 pi x / L)."""
+    import math
+
+    import paper_2301_05581_b200 as nufi
+
+    grid = nufi.GridSpec(d=1, L=4 * math.pi, Nx=32, Nv=8, vmax=1.0)
+    x = np.arange(32) * grid.hx
+    rho = np.cos(2 * math.pi * x / grid.L)
+    phi, _ = nufi.solve_poisson(nufi.DensityGrid(grid, rho))
+    ref = (grid.L / (2 * math.pi)) ** 2 * rho
+    assert np.abs(phi - ref).max() <= 1e-14 * np.abs(ref).max()
