@@ -23,6 +23,9 @@ constexpr double MAGIC = 6755399441055744.0;
 constexpr double GAUSS_NORM = 0.3989422804014327;  // 1/sqrt(2*pi), initial.py:22
 
 constexpr int MAX_D = 3;
+#ifndef NUFI_BARRIER_SLEEP_NS
+#define NUFI_BARRIER_SLEEP_NS 32
+#endif
 constexpr int MAX_FIELD_NODES = 4096;  // single-CTA field update limit (Nx^d)
 
 // ----------------------------------------------------------------------------
@@ -151,19 +154,19 @@ __device__ __forceinline__ void tma_bulk_g2s(void *dst_smem, const void *src_gme
 }
 
 // Grid-wide barrier for a cooperative (co-resident) launch: monotonically
-// increasing arrival counter, `target` = CTAs x barrier-generation.
+// increasing arrival counter, `target` = CTAs x barrier-generation.  Arrival is a
+// release-ordered reduction (no returned value, no separate fence); the wait is an
+// acquire-load spin.  The CTA barriers on both sides order the other threads.
 __device__ __forceinline__ void grid_barrier(unsigned *counter, unsigned target) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(counter, 1u);
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
         unsigned v;
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
         while (v < target) {
-            __nanosleep(64);  // back off: do not hammer the counter's L2 slice while others trace
+            __nanosleep(NUFI_BARRIER_SLEEP_NS);
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
         }
-        __threadfence();
     }
     __syncthreads();
 }
