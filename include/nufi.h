@@ -144,6 +144,21 @@ int nufi_step_finish(nufi_handle *h, int64_t n, const double *partials, double *
 int nufi_step_finish_async(nufi_handle *h, int64_t n, const double *partials, double *rho_out, double *E_out,
                            double *W_out, double *stats3);
 int nufi_check_status(nufi_handle *h);
+/* Multi-rank d = 1 runs with the exchange FUSED into the persistent kernel (no NCCL,
+ * no host loop): every rank's kernel stores its block sums straight into every peer's
+ * exchange table over NVLink (CUDA IPC peer memory), raises one arrival flag per peer
+ * (release, system scope) and waits for all peers' flags, then runs the identical tail.
+ * nufi_mg_setup: the handle's block range must be rank's share of B (B % world == 0);
+ * writes this rank's IPC handle (nufi_mg_handle_size() bytes) to ipc_handle_out.
+ * emulate != 0: all `world` ranks are CTA groups of ONE cooperative launch on this device
+ * (handle covers all blocks) -- the same protocol, for testing on one GPU.
+ * nufi_mg_connect: the world x nufi_mg_handle_size() bytes of all ranks' handles
+ * (e.g. all-gathered); afterwards nufi_run runs the fused multi-rank kernel.  A rank
+ * that never arrives trips a 4 s watchdog: nufi_run returns NUFI_ERR_COMM. */
+int nufi_mg_setup(nufi_handle *h, int world, int rank, int emulate, void *ipc_handle_out);
+int nufi_mg_connect(nufi_handle *h, const void *ipc_handles);
+int nufi_mg_handle_size(void);
+
 /* Fixed-order combine of the (allreduced) block partials -> rho, stats3. */
 int nufi_rho_finish(nufi_handle *h, const double *partials, double *rho_out, double *stats3);
 int64_t nufi_partials_len(nufi_handle *h); /* v_blocks * (Nx^d + 2) */

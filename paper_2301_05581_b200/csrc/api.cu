@@ -112,6 +112,15 @@ struct nufi_handle {
     size_t run_elems = 0;
     // observable sweep: per-CTA moment rows + the reduced vector (lazily allocated)
     double *mom_part = nullptr, *d_mom = nullptr;
+    // multi-rank run with the exchange fused into the persistent d = 1 kernel
+    int mg_world = 1, mg_rank = 0, mg_emulated = 0;
+    unsigned mg_steps = 0;            // arrival-flag base (steps run so far in mg mode)
+    void *mg_own = nullptr;           // cudaMalloc'd: exchange table (2 x stride) + G flags
+    void *mg_peer[NUFI_MG_MAX] = {};  // every rank's buffer (own / IPC-opened / emulated)
+    bool mg_opened[NUFI_MG_MAX] = {};
+    double *mg_part[NUFI_MG_MAX] = {}, *mg_fmm[NUFI_MG_MAX] = {};  // emulated ranks' partials
+    unsigned *mg_bar[NUFI_MG_MAX] = {};
+    int *mg_error = nullptr;
 
     int64_t len = 0;  // host mirror of the history length
     int f32 = 0;      // NUFI_FLAG_F32_HISTORY
@@ -294,7 +303,9 @@ static void choose_tiling(nufi_handle *h) {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
         const int64_t nt = (h->nodes + 31) / 32;
-        while (warps > 1 && (h->V / (warps / 2)) * nt <= sms && per_block % (warps / 2) == 0) warps >>= 1;
+        // the rows THIS handle traces (a rank of a sharded run traces b_hi - b_lo blocks)
+        const int64_t rows = per_block * (h->b_hi - h->b_lo);
+        while (warps > 1 && (rows / (warps / 2)) * nt <= sms && per_block % (warps / 2) == 0) warps >>= 1;
     }
     while (ppt > 1 && (per_block % (warps * ppt) != 0)) ppt >>= 1;
     while (passes > 1 && (per_block % ((int64_t)warps * ppt * passes) != 0)) passes >>= 1;
@@ -516,6 +527,15 @@ int nufi_destroy(nufi_handle *h) {
                     (void *)h->d_status, (void *)h->d_len, (void *)h->run_dev, (void *)h->tables,
                     (void *)h->ticket, (void *)h->barrier, (void *)h->mom_part, (void *)h->d_mom})
         if (p) cudaFreeAsync(p, h->stream);
+    for (int q = 0; q < NUFI_MG_MAX; ++q) {
+        if (h->mg_opened[q]) cudaIpcCloseMemHandle(h->mg_peer[q]);
+        else if (h->mg_peer[q] && h->mg_peer[q] != h->mg_own) cudaFree(h->mg_peer[q]);
+        if (q > 0 && h->mg_part[q]) cudaFree(h->mg_part[q]);
+        if (q > 0 && h->mg_fmm[q]) cudaFree(h->mg_fmm[q]);
+        if (h->mg_bar[q] && h->mg_bar[q] != h->barrier) cudaFree(h->mg_bar[q]);
+    }
+    if (h->mg_own) cudaFree(h->mg_own);
+    if (h->mg_error) cudaFree(h->mg_error);
     cudaStreamSynchronize(h->stream);  // frees complete -> the pool can hand the memory to the next handle
     pinned_put(h->run_host, h->run_elems);
     if (h->own_stream) cudaStreamDestroy(h->stream);
@@ -916,6 +936,79 @@ int nufi_check_status(nufi_handle *h) {
     return NUFI_OK;
 }
 
+// ---- multi-rank d = 1 runs with the exchange fused into the persistent kernel ----
+
+static size_t mg_xstride(const nufi_handle *h) { return (size_t)h->B * h->nodes + 2 * (size_t)h->B; }
+static size_t mg_bytes(const nufi_handle *h) {
+    return 2 * mg_xstride(h) * sizeof(double) + 256 + NUFI_MG_MAX * sizeof(unsigned);
+}
+static double *mg_table(void *buf) { return reinterpret_cast<double *>(buf); }
+static unsigned *mg_flags(const nufi_handle *h, void *buf) {
+    return reinterpret_cast<unsigned *>(reinterpret_cast<char *>(buf) + 2 * mg_xstride(h) * sizeof(double) + 128);
+}
+
+int nufi_mg_setup(nufi_handle *h, int world, int rank, int emulate, void *ipc_handle_out) {
+    CHECK_HANDLE(h);
+    if (h->d != 1) return fail(NUFI_ERR_USAGE, "the fused multi-rank run is the d = 1 persistent kernel");
+    if (world < 2 || world > NUFI_MG_MAX || rank < 0 || rank >= world)
+        return fail(NUFI_ERR_USAGE, "world must be 2..8 and 0 <= rank < world");
+    if (h->B % world) return fail(NUFI_ERR_USAGE, "v_blocks must be a multiple of the rank count");
+    if (h->mg_own) return fail(NUFI_ERR_USAGE, "multi-rank mode already set up");
+    if (emulate) {
+        if (h->b_lo != 0 || h->b_hi != h->B)
+            return fail(NUFI_ERR_USAGE, "an emulated run covers all velocity blocks");
+    } else if (h->b_lo != rank * (h->B / world) || h->b_hi != (rank + 1) * (h->B / world)) {
+        return fail(NUFI_ERR_USAGE, "handle block range does not match this rank's share");
+    }
+    CU(cudaStreamSynchronize(h->stream));
+    CU(cudaMalloc(&h->mg_own, mg_bytes(h)));  // plain cudaMalloc: IPC-exportable
+    CU(cudaMemset(h->mg_own, 0, mg_bytes(h)));
+    CU(cudaMalloc(&h->mg_error, sizeof(int)));
+    CU(cudaMemset(h->mg_error, 0, sizeof(int)));
+    h->mg_world = world;
+    h->mg_rank = emulate ? 0 : rank;
+    h->mg_emulated = emulate ? 1 : 0;
+    h->mg_steps = 0;
+    h->mg_peer[h->mg_rank] = h->mg_own;
+    if (emulate) {
+        const size_t pbytes = 2 * (size_t)h->vt_total * h->node_tiles * 32 * sizeof(double);
+        const size_t fbytes = 2 * (size_t)h->vt_total * h->node_tiles * 2 * sizeof(double);
+        h->mg_part[0] = h->partial;
+        h->mg_fmm[0] = h->fminmax;
+        for (int q = 0; q < world; ++q) {
+            if (q > 0) {
+                CU(cudaMalloc(&h->mg_peer[q], mg_bytes(h)));
+                CU(cudaMemset(h->mg_peer[q], 0, mg_bytes(h)));
+                CU(cudaMalloc(&h->mg_part[q], pbytes));
+                CU(cudaMalloc(&h->mg_fmm[q], fbytes));
+            }
+            CU(cudaMalloc(&h->mg_bar[q], sizeof(unsigned)));
+        }
+    } else if (ipc_handle_out) {
+        cudaIpcMemHandle_t ipc;
+        CU(cudaIpcGetMemHandle(&ipc, h->mg_own));
+        memcpy(ipc_handle_out, &ipc, sizeof ipc);
+    }
+    return NUFI_OK;
+}
+
+int nufi_mg_connect(nufi_handle *h, const void *ipc_handles) {
+    CHECK_HANDLE(h);
+    if (!h->mg_own || h->mg_emulated) return fail(NUFI_ERR_USAGE, "call nufi_mg_setup (real mode) first");
+    if (!ipc_handles) return fail(NUFI_ERR_USAGE, "null handles");
+    for (int q = 0; q < h->mg_world; ++q) {
+        if (q == h->mg_rank) continue;
+        cudaIpcMemHandle_t ipc;
+        memcpy(&ipc, reinterpret_cast<const char *>(ipc_handles) + q * sizeof(cudaIpcMemHandle_t), sizeof ipc);
+        cudaError_t e = cudaIpcOpenMemHandle(&h->mg_peer[q], ipc, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return fail(NUFI_ERR_COMM, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+        h->mg_opened[q] = true;
+    }
+    return NUFI_OK;
+}
+
+int nufi_mg_handle_size(void) { return (int)sizeof(cudaIpcMemHandle_t); }
+
 int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, double *W_hist, double *stats_hist,
              int64_t *evals) {
     CHECK_HANDLE(h);
@@ -969,6 +1062,25 @@ int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, d
         // two-level combine when every CTA re-reading all tile partials would dominate the tail
         P.two_level = (int64_t)h->vt_total * h->nodes > 16384 ? 1 : 0;
         if (const char *e = getenv("NUFI_TWO_LEVEL")) P.two_level = atoi(e);
+        if (h->mg_world > 1) {
+            if (!h->mg_emulated)
+                for (int q = 0; q < h->mg_world; ++q)
+                    if (!h->mg_peer[q]) return fail(NUFI_ERR_USAGE, "multi-rank run: call nufi_mg_connect first");
+            P.two_level = 0;
+            P.mg_ranks = h->mg_world;
+            P.mg_emulated = h->mg_emulated;
+            P.mg_rank = h->mg_rank;
+            P.mg_base = h->mg_steps;
+            P.mg_error = h->mg_error;
+            for (int q = 0; q < h->mg_world; ++q) {
+                P.mg_xtab[q] = mg_table(h->mg_peer[q]);
+                P.mg_flags[q] = mg_flags(h, h->mg_peer[q]);
+                P.mg_partial[q] = h->mg_part[q];
+                P.mg_fminmax[q] = h->mg_fmm[q];
+                P.mg_barrier[q] = h->mg_bar[q];
+                if (h->mg_emulated && h->mg_bar[q]) CU(cudaMemsetAsync(h->mg_bar[q], 0, sizeof(unsigned), h->stream));
+            }
+        }
         static const char *stamp_path = getenv("NUFI_STAMPS");  // debug: per-step phase timestamps
         unsigned long long *stamps = nullptr;
         if (stamp_path) CU(cudaMalloc(&stamps, (3 * steps + 10 + 6 * 1024) * sizeof(unsigned long long)));
@@ -1030,6 +1142,12 @@ int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, d
     }
     int rc = check_status(h, "solve_poisson");  // synchronises
     if (rc) return rc;
+    if (h->mg_world > 1 && h->d == 1 && !nopersist) {
+        int err = 0;
+        CU(cudaMemcpy(&err, h->mg_error, sizeof(int), cudaMemcpyDeviceToHost));
+        if (err) return fail(NUFI_ERR_COMM, "multi-rank run: a peer rank did not arrive within 4 s (watchdog)");
+        h->mg_steps += (unsigned)steps;  // every rank runs the same sequence: identical bases
+    }
     h->len = n_last + 1;
     for (int q = 0; q < 4; ++q)
         if (user[q] && !dev[q]) memcpy(user[q], base_host[q], steps * width[q] * sizeof(double));

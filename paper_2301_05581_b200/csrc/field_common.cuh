@@ -60,6 +60,8 @@ struct FieldParams {
     unsigned long long *tstamps;  // debug: phase timestamps (thread 0), 10 slots
 };
 
+#define NUFI_MG_MAX 8
+
 // d = 1 whole-run persistent kernel (run_1d.cu)
 struct Run1DParams {
     TraceRhoParams tp;  // geometry / arithmetic (tp.n unused)
@@ -71,6 +73,18 @@ struct Run1DParams {
     unsigned long long *stamps;                       // optional: CTA 0 globaltimer per step x 3
     double *blocks;   // two-level combine: B * nodes block sums + B (min, max)
     int two_level;    // combine tile partials across the grid first (second grid barrier)
+    // ---- multi-rank run with the exchange fused into the kernel (run_1d.cu) ----
+    int mg_ranks;          // G ranks (1: single GPU)
+    int mg_emulated;       // 1: the G ranks are CTA groups of this one cooperative launch
+    int mg_rank;           // real mode: this launch's rank
+    int mg_ctas;           // CTAs per rank
+    unsigned mg_base;      // arrival-flag value before this run's first step (monotonic)
+    int *mg_error;         // watchdog: set when a peer never arrives (device flag)
+    double *mg_xtab[NUFI_MG_MAX];     // per rank: exchange table, 2 x (B Nx + 2B) doubles (step parity)
+    unsigned *mg_flags[NUFI_MG_MAX];  // per rank: G arrival flags, slot q written by rank q
+    // per-rank local buffers in emulated mode (real mode: tp.partial / tp.fminmax / barrier)
+    double *mg_partial[NUFI_MG_MAX], *mg_fminmax[NUFI_MG_MAX];
+    unsigned *mg_barrier[NUFI_MG_MAX];
 };
 
 #define NUFI_STAMP(p, k)                                                              \

@@ -81,6 +81,17 @@ __global__ void __launch_bounds__(288, 2) run_1d_kernel(const Run1DParams P) {
     const int stages = p.stages;
     const int nodes = p.nodes;
 
+    // multi-rank context: rank rk of G traces its blocks' tiles with nct CTAs (lc local index)
+    const int G = P.mg_ranks > 1 ? P.mg_ranks : 1;
+    const bool mg = G > 1, emu = mg && P.mg_emulated;
+    const int rk = !mg ? 0 : (emu ? (int)blockIdx.x / P.mg_ctas : P.mg_rank);
+    const int lc = emu ? (int)blockIdx.x % P.mg_ctas : (int)blockIdx.x;
+    const int nct = emu ? P.mg_ctas : (int)gridDim.x;
+    double *const my_partial = emu ? P.mg_partial[rk] : p.partial;
+    double *const my_fminmax = emu ? P.mg_fminmax[rk] : p.fminmax;
+    unsigned *const my_barrier = emu ? P.mg_barrier[rk] : P.barrier;
+    const int tiles_r = P.tiles / G, tile_lo = rk * tiles_r;
+
     // shared memory: [ring | tail workspace (aliased)] | barriers | red | local slab.
     // The tail runs between grid barriers when no bulk copy is in flight (every copy
     // of a step is consumed before its barrier), so it reuses the ring's bytes;
@@ -116,11 +127,12 @@ __global__ void __launch_bounds__(288, 2) run_1d_kernel(const Run1DParams P) {
         const int groups = (m + SPS - 1) / SPS;
         // partials double-buffered by step parity: a CTA that finished the tail of
         // step n may write step n+1's partials while a slower one still reads step n's
-        double *part = p.partial + (size_t)(n & 1) * P.tiles * 32;
-        double *fmm = p.fminmax + (size_t)(n & 1) * P.tiles * 2;
+        double *part = my_partial + (size_t)(n & 1) * P.tiles * 32;
+        double *fmm = my_fminmax + (size_t)(n & 1) * P.tiles * 2;
         const int top_cnt = m - (groups - 1) * SPS;
 
-        for (int tile = blockIdx.x; tile < P.tiles; tile += gridDim.x) {
+        for (int t_loc = lc; t_loc < tiles_r; t_loc += nct) {
+            const int tile = tile_lo + t_loc;
             static constexpr bool kAlt = false;  // tile mapping: v-tile-major (true) or node-tile-major
             const int vts = P.tiles / p.node_tiles;
             const int nt = kAlt ? tile / vts : tile % p.node_tiles;
@@ -231,13 +243,98 @@ __global__ void __launch_bounds__(288, 2) run_1d_kernel(const Run1DParams P) {
             P.stamps[3 * (P.n_last - P.n_first + 1) + 10 + (n / 400 - 1) * 1024 + blockIdx.x] =
                 (globaltimer() << 8) | (smid & 0xff);
         }
-        grid_barrier(P.barrier, ++gen * gridDim.x);
+        grid_barrier(my_barrier, ++gen * nct);
         if (P.stamps && blockIdx.x == 0 && threadIdx.x == 0) P.stamps[3 * (n - P.n_first) + 1] = globaltimer();
 
         FieldParams fp = P.fp;
         fp.sums = part;
         fp.minmax = fmm;
-        if (P.two_level) {
+        if (mg) {
+            // ---- fused exchange over peer memory: this rank's block sums (the canonical
+            // sequential order over the block's tile rows) and block (min, max) are stored
+            // straight into EVERY rank's exchange table (NVLink stores; parity-buffered by
+            // step), then one arrival flag per peer (release, system scope) and a wait for
+            // all peers' flags (acquire).  Every rank then runs the identical tail on the
+            // identical table, so all ranks hold bit-identical histories.
+            const int B = fp.B, rpb = fp.rows_per_block, nb = B / G, b_lo = rk * nb;
+            const size_t xstride = (size_t)B * nodes + 2 * (size_t)B, xoff = (size_t)(n & 1) * xstride;
+            bool wrote = false;
+            for (int64_t o = (int64_t)lc * blockDim.x + threadIdx.x; o < (int64_t)nb * nodes;
+                 o += (int64_t)nct * blockDim.x) {
+                const int b = b_lo + (int)(o / nodes), i = (int)(o - (o / nodes) * nodes);
+                const double *src = part + (size_t)b * rpb * nodes + i;
+                double Sb = 0.0;
+                int q = 0;
+                for (; q + 8 <= rpb; q += 8) {
+                    double v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (size_t)(q + u) * nodes);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) Sb += v[u];
+                }
+                for (; q < rpb; ++q) Sb += __ldcg(src + (size_t)q * nodes);
+                for (int r = 0; r < G; ++r) P.mg_xtab[r][xoff + (size_t)b * nodes + i] = Sb;
+                wrote = true;
+            }
+            for (int bb = lc; bb < nb; bb += nct) {
+                const int b = b_lo + bb;
+                double mn = DBL_MAX, mx = -DBL_MAX;
+                for (int q = threadIdx.x; q < fp.mm_per_block; q += blockDim.x) {
+                    mn = fmin(mn, __ldcg(fmm + 2 * ((size_t)b * fp.mm_per_block + q)));
+                    mx = fmax(mx, __ldcg(fmm + 2 * ((size_t)b * fp.mm_per_block + q) + 1));
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                }
+                if (lane == 0) {
+                    red[warp] = mn;
+                    red[32 + warp] = mx;
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+                        mn = fmin(mn, red[w]);
+                        mx = fmax(mx, red[32 + w]);
+                    }
+                    for (int r = 0; r < G; ++r) {
+                        P.mg_xtab[r][xoff + (size_t)B * nodes + 2 * b] = mn;
+                        P.mg_xtab[r][xoff + (size_t)B * nodes + 2 * b + 1] = mx;
+                    }
+                    wrote = true;
+                }
+                __syncthreads();
+            }
+            if (wrote) __threadfence_system();  // this thread's peer stores before the flags
+            grid_barrier(my_barrier, ++gen * nct);
+            if (lc == 0 && threadIdx.x == 0) {
+                const unsigned target = P.mg_base + (unsigned)(n - P.n_first) + 1u;
+                for (int r = 0; r < G; ++r)
+                    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(P.mg_flags[r] + rk), "r"(target)
+                                 : "memory");
+                const unsigned long long t0 = globaltimer();
+                for (int q = 0; q < G; ++q) {
+                    unsigned v;
+                    for (;;) {
+                        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(P.mg_flags[rk] + q)
+                                     : "memory");
+                        if (v >= target) break;
+                        if (globaltimer() - t0 > 4000000000ull) {  // 4 s: a peer is gone
+                            *P.mg_error = 1;
+                            break;
+                        }
+                        __nanosleep(NUFI_BARRIER_SLEEP_NS);
+                    }
+                }
+            }
+            grid_barrier(my_barrier, ++gen * nct);
+            if (*(volatile int *)P.mg_error) break;  // identical decision in every CTA of the rank
+            fp.sums = P.mg_xtab[rk] + xoff;
+            fp.rows_per_block = 1;
+            fp.minmax = fp.sums + (size_t)B * nodes;
+            fp.mm_per_block = 1;
+        } else if (P.two_level) {
             // level 1, spread over the grid: tile partials -> block sums in the SAME
             // sequential order the tail uses (field_update_1d_body), block (min, max)
             const int B = fp.B, rpb = fp.rows_per_block;
@@ -295,7 +392,7 @@ __global__ void __launch_bounds__(288, 2) run_1d_kernel(const Run1DParams P) {
         fp.slot = n;
         fp.ev_local = slabN;
         const int64_t row = n - P.n_first;
-        if (blockIdx.x == 0) {
+        if (lc == 0 && !(emu && rk != 0)) {  // one publisher per rank (emulated: rank 0 only)
             fp.rho_out = P.rho_hist ? P.rho_hist + row * nodes : nullptr;
             fp.E_out = P.E_hist ? P.E_hist + row * nodes : nullptr;
             fp.W_out = P.W_hist ? P.W_hist + row : nullptr;
@@ -328,19 +425,31 @@ static cudaError_t launch_run(const Run1DParams &P, int threads, int device, cud
     auto kern = run_1d_kernel<NX, SPS>;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const int G = P.mg_ranks > 1 ? P.mg_ranks : 1;
+    const bool emu = G > 1 && P.mg_emulated;
+    // tiles this launch traces (emulated: all ranks' tiles in one launch)
+    const int tiles_launch = (G > 1 && !emu) ? P.tiles / G : P.tiles;
     size_t smem = run_1d_smem_bytes(P.tp, threads);
     // latency-bound (tiles <= SMs): one CTA per SM -- reserve more than half the
     // SM's shared memory so the scheduler cannot double up CTAs on one SM
-    if (P.tiles <= sms && smem < 120 * 1024) smem = 120 * 1024;
+    if (tiles_launch <= sms && smem < 120 * 1024) smem = 120 * 1024;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    const int grid = std::min(P.tiles, per_sm * sms);
-    if (grid_out) *grid_out = grid;
     Run1DParams args = P;
+    int grid;
+    if (emu) {  // G equal CTA groups, every CTA co-resident
+        args.mg_ctas = std::min(P.tiles / G, (per_sm * sms) / G);
+        if (args.mg_ctas < 1) return cudaErrorInvalidConfiguration;
+        grid = G * args.mg_ctas;
+    } else {
+        grid = std::min(tiles_launch, per_sm * sms);
+        args.mg_ctas = grid;
+    }
+    if (grid_out) *grid_out = grid;
     void *kargs[] = {&args};
     return cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(threads), kargs, smem, st);
 }

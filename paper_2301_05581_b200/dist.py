@@ -21,6 +21,7 @@ ranks (gloo) with a reference implementation of the block sums.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -97,6 +98,32 @@ class DistributedSimulation:
         n = int(self.history.handle.lib.nufi_partials_len(self.history.handle.h))
         self.partials = torch.zeros(n, dtype=torch.float64, device=f"cuda:{device}")
         self.block_lo, self.block_hi = lo, hi
+        self.fused = False
+        if grid.d == 1 and self.world > 1 and B % self.world == 0 and os.environ.get("NUFI_MG", "1") != "0":
+            self._connect_fused(device)
+
+    def _connect_fused(self, device: int) -> None:
+        """d = 1: the persistent kernel with the exchange fused in (nufi_mg_*): every rank
+        exports its exchange buffer (CUDA IPC), the handles are all-gathered over the
+        process group, every rank opens its peers'.  Falls back to the per-step NCCL
+        loop (with a warning) if peer memory is unavailable."""
+        import warnings
+
+        h = self.history.handle
+        try:
+            size = int(h.lib.nufi_mg_handle_size())
+            buf = ctypes.create_string_buffer(size)
+            h.call("nufi_mg_setup", self.world, self.rank, 0, buf)
+            mine = self.torch.tensor(list(buf.raw), dtype=self.torch.uint8, device=f"cuda:{device}")
+            allh = [self.torch.empty_like(mine) for _ in range(self.world)]
+            self.dist.all_gather(allh, mine, group=self.group)
+            blob = bytes(b for t in allh for b in t.cpu().tolist())
+            h.call("nufi_mg_connect", blob)
+            self.dist.barrier(group=self.group)  # every rank connected before any kernel runs
+            self.fused = True
+        except Exception as exc:  # pragma: no cover - depends on the machine's peer access
+            warnings.warn(f"fused multi-rank kernel unavailable ({exc}); using the per-step NCCL loop")
+            self.fused = False
 
     def step(self, outputs: dict | None = None, row: int = 0, sync: bool = True):
         """One step: trace own blocks -> allreduce -> redundant field update."""
@@ -131,6 +158,22 @@ class DistributedSimulation:
         like Simulation.run)."""
         first = len(self.history)
         steps = self.n_steps + 1 - first
+        if self.fused:
+            # one persistent kernel per rank, exchanging over peer memory every step
+            from . import _lib
+
+            self.dist.barrier(group=self.group)  # start together (the kernels wait on each other)
+            g = self.grid
+            if outputs is None:
+                outputs = dict(rho=np.empty((steps, g.n_nodes)), E=np.empty((steps, g.n_nodes, g.d)),
+                               W=np.empty(steps), stats=np.empty((steps, 3)))
+            ev = ctypes.c_int64(0)
+            self.history.handle.call("nufi_run", self.n_steps, _lib.ptr(outputs.get("rho")),
+                                     _lib.ptr(outputs.get("E")), _lib.ptr(outputs.get("W")),
+                                     _lib.ptr(outputs.get("stats")), ctypes.byref(ev))
+            # nufi_run counts the whole grid; this rank traced its share of the blocks
+            self.ctx.field_evals += int(ev.value) * (self.block_hi - self.block_lo) // self.B
+            return outputs
         host = outputs is None
         if host:
             g = self.grid

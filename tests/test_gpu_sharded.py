@@ -121,3 +121,45 @@ def test_distributed_simulation_nccl_single_rank(name, N):
         assert np.array_equal(host["rho"], ref.rho) and np.array_equal(host["W"], ref.W)
     finally:
         dist.destroy_process_group()
+
+
+def _emulated_mg_run(name, N, world, repeat=1):
+    w = workload(name)
+    sim = nufi.Simulation(w.grid, w.ic, w.tau, N, v_blocks=8)
+    h = sim.history.handle
+    h.call("nufi_mg_setup", world, 0, 1, None)  # all ranks as CTA groups of one launch
+    res = None
+    for _ in range(repeat):  # repeated runs: the arrival flags keep counting across runs
+        sim.history.truncate(0)
+        res = sim.run()
+    return sim, res
+
+
+@pytest.mark.parametrize("name,N", [("kat_wl", 60), ("ts1", 200), ("rag1", 20)])
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_fused_multirank_kernel_emulated(name, N, world):
+    """The fused multi-rank persistent kernel (exchange over peer memory + arrival flags,
+    run_1d.cu) with `world` ranks emulated as CTA groups of one cooperative launch:
+    bit-identical to the single-GPU run (same tiles, same block-combine order)."""
+    w = workload(name)
+    if (w.grid.n_cells % 8) or (8 % world):
+        pytest.skip("needs 8 velocity blocks divisible by the rank count")
+    ref_sim = nufi.Simulation(w.grid, w.ic, w.tau, N, v_blocks=8)
+    ref = ref_sim.run()
+    sim, res = _emulated_mg_run(name, N, world, repeat=2)
+    assert np.array_equal(res.rho, ref.rho), np.abs(res.rho - ref.rho).max()
+    assert np.array_equal(res.W, ref.W)
+    assert np.array_equal(sim.history.stacked(), ref_sim.history.stacked())
+
+
+def test_fused_multirank_setup_errors():
+    w = workload("kat_wl")
+    h = nufi.PotentialHistory(w.grid, w.tau, capacity=4, v_blocks=8, block_range=(0, 4))
+    with pytest.raises(nufi.UsageError):
+        h.handle.call("nufi_mg_setup", 2, 1, 0, None)  # rank 1's share is blocks 4..8
+    with pytest.raises(nufi.UsageError):
+        h.handle.call("nufi_mg_setup", 2, 0, 1, None)  # emulation needs all blocks
+    w2 = workload("tiny2")
+    h2 = nufi.PotentialHistory(w2.grid, w2.tau, capacity=4, v_blocks=8)
+    with pytest.raises(nufi.UsageError):
+        h2.handle.call("nufi_mg_setup", 2, 0, 1, None)  # d = 1 only
