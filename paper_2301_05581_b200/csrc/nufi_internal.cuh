@@ -171,6 +171,22 @@ __device__ __forceinline__ void grid_barrier(unsigned *counter, unsigned target)
     __syncthreads();
 }
 
+// The same barrier for a rank of a fused multi-rank run: gives up (returns) when the
+// rank's error flag is raised, so a watchdog timeout cannot strand the other CTAs.
+__device__ __forceinline__ void grid_barrier_wd(unsigned *counter, unsigned target, const int *err) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
+        unsigned v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+        while (v < target && *(volatile const int *)err == 0) {
+            __nanosleep(NUFI_BARRIER_SLEEP_NS);
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+        }
+    }
+    __syncthreads();
+}
+
 // ----------------------------------------------------------------------------
 // kernel parameter blocks
 // ----------------------------------------------------------------------------

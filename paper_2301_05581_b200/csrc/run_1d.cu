@@ -243,7 +243,12 @@ __global__ void __launch_bounds__(288, 2) run_1d_kernel(const Run1DParams P) {
             P.stamps[3 * (P.n_last - P.n_first + 1) + 10 + (n / 400 - 1) * 1024 + blockIdx.x] =
                 (globaltimer() << 8) | (smid & 0xff);
         }
-        grid_barrier(my_barrier, ++gen * nct);
+        if (mg) {
+            grid_barrier_wd(my_barrier, ++gen * nct, P.mg_error);
+            if (*(volatile int *)P.mg_error) break;
+        } else {
+            grid_barrier(my_barrier, ++gen * nct);
+        }
         if (P.stamps && blockIdx.x == 0 && threadIdx.x == 0) P.stamps[3 * (n - P.n_first) + 1] = globaltimer();
 
         FieldParams fp = P.fp;
@@ -306,13 +311,17 @@ __global__ void __launch_bounds__(288, 2) run_1d_kernel(const Run1DParams P) {
                 }
                 __syncthreads();
             }
-            if (wrote) __threadfence_system();  // this thread's peer stores before the flags
-            grid_barrier(my_barrier, ++gen * nct);
-            if (lc == 0 && threadIdx.x == 0) {
-                const unsigned target = P.mg_base + (unsigned)(n - P.n_first) + 1u;
+            // Cross-rank arrival without further grid barriers: after its peer stores (ordered
+            // by the CTA barrier and one cumulative system-scope fence) every CTA adds 1 to its
+            // rank's slot of EVERY rank's arrival counter, then waits until each slot of its
+            // own rank's counters shows all nct CTAs of that peer for this step.
+            (void)wrote;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                asm volatile("fence.sc.sys;" ::: "memory");
                 for (int r = 0; r < G; ++r)
-                    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(P.mg_flags[r] + rk), "r"(target)
-                                 : "memory");
+                    asm volatile("red.relaxed.sys.global.add.u32 [%0], 1;" ::"l"(P.mg_flags[r] + rk) : "memory");
+                const unsigned target = (P.mg_base + (unsigned)(n - P.n_first) + 1u) * (unsigned)nct;
                 const unsigned long long t0 = globaltimer();
                 for (int q = 0; q < G; ++q) {
                     unsigned v;
@@ -321,14 +330,14 @@ __global__ void __launch_bounds__(288, 2) run_1d_kernel(const Run1DParams P) {
                                      : "memory");
                         if (v >= target) break;
                         if (globaltimer() - t0 > 4000000000ull) {  // 4 s: a peer is gone
-                            *P.mg_error = 1;
+                            atomicExch(P.mg_error, 1);
                             break;
                         }
                         __nanosleep(NUFI_BARRIER_SLEEP_NS);
                     }
                 }
             }
-            grid_barrier(my_barrier, ++gen * nct);
+            __syncthreads();
             if (*(volatile int *)P.mg_error) break;  // identical decision in every CTA of the rank
             fp.sums = P.mg_xtab[rk] + xoff;
             fp.rows_per_block = 1;
