@@ -100,3 +100,26 @@ def test_validation_errors_without_gpu():
     cfg.k = 0.3
     with pytest.raises(UsageError, match="multiple of 2\\*pi"):
         _lib.Handle(cfg, 0)
+
+
+def test_size_limits_without_gpu():
+    """Maximum sizes: the single-CTA field update takes Nx^d <= 4096 (every BASELINE grid;
+    wl3 = 16^3 is exactly the limit); larger grids are refused with ConfigError before any
+    device work, as are unknown flags and v_blocks that do not divide Nv^d."""
+    from paper_2301_05581_b200.configs import workload
+    from paper_2301_05581_b200.errors import ConfigError, UsageError
+
+    w = workload("wl3")
+    cfg = _lib.make_config(w.grid, w.ic, w.tau, 10)
+    cfg.Nx = 17  # 4913 nodes
+    with pytest.raises(ConfigError, match="single-CTA field update limit"):
+        _lib.Handle(cfg, 0)
+    w2 = workload("wl2")
+    cfg = _lib.make_config(w2.grid, w2.ic, w2.tau, 10)
+    cfg.Nx = 65  # 4225 nodes
+    with pytest.raises(ConfigError):
+        _lib.Handle(cfg, 0)
+    cfg = _lib.make_config(w2.grid, w2.ic, w2.tau, 10)
+    cfg.flags = 8
+    with pytest.raises(UsageError, match="flags"):
+        _lib.Handle(cfg, 0)
