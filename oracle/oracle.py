@@ -105,6 +105,14 @@ def case(name: str) -> Case:
     if name == "tiny3":
         streams = Profile(centers=(-2.4, 2.4), weights=(0.5, 0.5))
         return Case(3, 10.0 * math.pi, 8, 4, 6.0, 1 / 8, 1e-3, 0.2, (_MAX, streams, _MAX))
+    if name == "big1":
+        return Case(1, FOUR_PI, 5000, 16, 6.0, 1 / 8, 0.05, 0.5, (_MAX,))
+    if name == "big2":
+        return Case(2, FOUR_PI, 72, 6, 6.0, 1 / 8, 0.2, 0.5, (_MAX,) * 2)
+    if name == "big2g":
+        return Case(2, FOUR_PI, 120, 4, 6.0, 1 / 8, 0.2, 0.5, (_MAX,) * 2)
+    if name == "big3":
+        return Case(3, FOUR_PI, 22, 3, 5.0, 1 / 8, 0.05, 0.5, (_MAX,) * 3)
     if name == "rag1":
         return Case(1, FOUR_PI, 24, 40, 6.0, 1 / 8, 0.05, 0.5, (_MAX,))
     if name == "rag2":

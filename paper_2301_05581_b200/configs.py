@@ -69,6 +69,19 @@ def workload(name: str) -> Workload:
     if name == "rag3":
         return Workload(name, GridSpec(3, FOUR_PI, 5, 3, 5.0), weak_landau_3d(alpha=0.05), 1 / 8, 8,
                         "d=3 Landau, 5^3 x 3^3")
+    # grids beyond one CTA
+    if name == "big1":
+        return Workload(name, GridSpec(1, FOUR_PI, 5000, 16, 6.0), make_benchmark("weak_landau_1d", alpha=0.05), 1 / 8,
+                        6, "d=1 Nx=5000")
+    if name == "big2":
+        return Workload(name, GridSpec(2, FOUR_PI, 72, 6, 6.0), make_benchmark("strong_landau_2d", alpha=0.2), 1 / 8,
+                        6, "d=2 72^2 x 6^2")
+    if name == "big2g":
+        return Workload(name, GridSpec(2, FOUR_PI, 120, 4, 6.0), make_benchmark("strong_landau_2d", alpha=0.2), 1 / 8,
+                        4, "d=2 120^2 x 4^2 (in-place trace)")
+    if name == "big3":
+        return Workload(name, GridSpec(3, FOUR_PI, 22, 3, 5.0), weak_landau_3d(alpha=0.05), 1 / 8, 4,
+                        "d=3 22^3 x 3^3 (in-place trace)")
     raise KeyError(name)
 
 

@@ -38,6 +38,10 @@ cudaError_t launch_eval_f0(int d, const F0Params &f0, const double *X, const dou
 cudaError_t launch_trace_rho_1d(const TraceRhoParams &p, const FieldParams &fp, int fuse, unsigned *ticket, int ctas,
                                 int threads, cudaStream_t st);
 int trace_rho_1d_sps(int N);
+cudaError_t launch_trace_rho_global(int d, bool mom, bool pow2, const TraceRhoParams &p, double K, int ctas,
+                                    int threads, cudaStream_t st);
+cudaError_t launch_field_large(const FieldParams &f, double *scratch, cudaStream_t st);
+size_t field_large_scratch_doubles(int nodes);
 cudaError_t launch_field_tables(double *tw, double *fac, double *k2, int d, int N, int nodes, double k_scale,
                                 cudaStream_t st);
 cudaError_t launch_run_1d(const Run1DParams &P, int threads, int device, cudaStream_t st, int *grid_out);
@@ -123,6 +127,9 @@ struct nufi_handle {
     int *mg_error = nullptr;
 
     int64_t len = 0;  // host mirror of the history length
+    bool large = false;   // Nx^d > MAX_FIELD_NODES: multi-CTA tail (field_large.cu)
+    bool gl = false;      // slabs too large for a shared-memory ring: traced in place (GL kernels)
+    double *large_scratch = nullptr;
     int f32 = 0;      // NUFI_FLAG_F32_HISTORY
 
     // optional per-launch event timing (nufi_profile)
@@ -272,8 +279,8 @@ static int validate(const nufi_config &c) {
         return fail(NUFI_ERR_USAGE, buf);  // initial.py:95-99
     }
     const long long nodes = (long long)std::pow((double)c.Nx, c.d);
-    if (nodes > MAX_FIELD_NODES) {
-        snprintf(buf, sizeof buf, "Nx^d = %lld exceeds the single-CTA field update limit %d", nodes, MAX_FIELD_NODES);
+    if (nodes > MAX_GRID_NODES) {
+        snprintf(buf, sizeof buf, "Nx^d = %lld exceeds the supported grid size %d", nodes, MAX_GRID_NODES);
         return fail(NUFI_ERR_CONFIG, buf);
     }
     const double V = std::pow((double)c.Nv, c.d);
@@ -336,6 +343,7 @@ static void choose_tiling(nufi_handle *h) {
         // keep the ring within the 227 KB per-CTA shared-memory limit
         while (h->sps > 1 && (size_t)h->stages * h->sps * slab_bytes > 200 * 1024) --h->sps;
         while (h->stages > 2 && (size_t)h->stages * h->sps * slab_bytes > 200 * 1024) --h->stages;
+        h->gl = (size_t)h->stages * h->sps * slab_bytes > 200 * 1024;  // even 2 x 1 slab does not fit
     }
 }
 
@@ -483,7 +491,9 @@ int nufi_create(const nufi_config *cfg, int device, void *stream, nufi_handle **
     }
     h->ev_elems = ev_slab_elems(c.d, c.Nx);
     h->f32 = (c.flags & NUFI_FLAG_F32_HISTORY) ? 1 : 0;
+    h->large = h->nodes > MAX_FIELD_NODES;
     choose_tiling(h);
+    if (h->large && h->d == 1) h->gl = true;  // d = 1 beyond one CTA: generic in-place trace
 
     const size_t nodes = h->nodes;
     CU(pool_init(device));
@@ -500,6 +510,7 @@ int nufi_create(const nufi_config *cfg, int device, void *stream, nufi_handle **
     CU(dalloc(&h->d_rho_bar, sizeof(double), h->stream));
     CU(dalloc(&h->d_status, sizeof(int), h->stream));
     CU(dalloc(&h->d_len, sizeof(int64_t), h->stream));
+    if (h->large) CU(dalloc(&h->large_scratch, field_large_scratch_doubles(h->nodes) * sizeof(double), h->stream));
     CU(dalloc(&h->tables, (4 * (size_t)h->N + 3 * nodes) * sizeof(double), h->stream));
     CU(dalloc(&h->ticket, sizeof(unsigned), h->stream));
     CU(dalloc(&h->barrier, sizeof(unsigned), h->stream));
@@ -525,7 +536,8 @@ int nufi_destroy(nufi_handle *h) {
     for (void *p : {(void *)h->hist, (void *)h->ev_hist, (void *)h->partial, (void *)h->fminmax, (void *)h->blocks,
                     (void *)h->d_rho, (void *)h->d_E, (void *)h->d_W, (void *)h->d_stats, (void *)h->d_rho_bar,
                     (void *)h->d_status, (void *)h->d_len, (void *)h->run_dev, (void *)h->tables,
-                    (void *)h->ticket, (void *)h->barrier, (void *)h->mom_part, (void *)h->d_mom})
+                    (void *)h->ticket, (void *)h->barrier, (void *)h->mom_part, (void *)h->d_mom,
+                    (void *)h->large_scratch})
         if (p) cudaFreeAsync(p, h->stream);
     for (int q = 0; q < NUFI_MG_MAX; ++q) {
         if (h->mg_opened[q]) cudaIpcCloseMemHandle(h->mg_peer[q]);
@@ -647,6 +659,15 @@ static TraceRhoParams trace_params(nufi_handle *h, int64_t n, int b_lo) {
 // CTA width of every d = 1 tail (see launch_field_update); 0 = by size for d >= 2
 static int field_threads(const nufi_handle *h) { return h->d == 1 ? h->threads + 32 : 0; }
 
+static FieldParams field_params(nufi_handle *h);
+
+// the step tail: one CTA (field_update_body) or, beyond MAX_FIELD_NODES, the multi-CTA
+// sequence of field_large.cu
+static cudaError_t enqueue_field(nufi_handle *h, const FieldParams &f) {
+    if (h->large) return launch_field_large(f, h->large_scratch, h->stream);
+    return launch_field_update(f, h->stream, field_threads(h));
+}
+
 static FieldParams field_params(nufi_handle *h) {
     FieldParams f{};
     f.d = h->d;
@@ -685,7 +706,12 @@ static int enqueue_trace(nufi_handle *h, int64_t n, int b_lo, int b_hi) {
     const TraceRhoParams p = trace_params(h, n, b_lo);
     const int ctas = (b_hi - b_lo) * h->vt_per_block * h->node_tiles;
     ProfScope ps(h, 0, point_steps(h, n, b_hi - b_lo));
-    if (h->d == 1) {
+    if (h->gl) {
+        TraceRhoParams q = p;
+        if (h->d >= 2) q.passes = h->passes * h->ppt;  // one point per thread, same rows
+        CU(launch_trace_rho_global(h->d, false, h->pow2, q, h->K, ctas, h->d == 1 ? 32 * h->vt_rows : h->threads,
+                                   h->stream));
+    } else if (h->d == 1) {
         FieldParams none{};
         CU(launch_trace_rho_1d(p, none, 0, h->ticket, ctas, h->threads + 32, h->stream));
     } else {
@@ -719,7 +745,7 @@ static int enqueue_step(nufi_handle *h, int64_t n, bool full, const StepOut &o) 
     f.E_out = o.E;
     f.finish_only = full ? 0 : 1;
     static const bool nofuse = getenv("NUFI_NOFUSE") != nullptr;
-    if (h->d == 1 && !nofuse) {
+    if (h->d == 1 && !nofuse && !h->large) {
         f.sums = h->partial;
         f.rows_per_block = h->vt_per_block;
         f.minmax = h->fminmax;
@@ -738,7 +764,7 @@ static int enqueue_step(nufi_handle *h, int64_t n, bool full, const StepOut &o) 
     f.minmax = h->blocks + (size_t)h->B * h->nodes;
     f.mm_per_block = 1;
     ProfScope ps(h, 2);
-    CU(launch_field_update(f, h->stream, field_threads(h)));
+    CU(enqueue_field(h, f));
     return NUFI_OK;
 }
 
@@ -805,7 +831,7 @@ int nufi_rho_finish(nufi_handle *h, const double *partials, double *rho_out, dou
     f.finish_only = 1;
     {
         ProfScope ps(h, 2);
-        CU(launch_field_update(f, h->stream, field_threads(h)));
+        CU(enqueue_field(h, f));
     }
     return copy_step_outputs(h, rho_out, nullptr, nullptr, stats3);
 }
@@ -835,7 +861,7 @@ int nufi_field_update(nufi_handle *h, const double *rho, double *W_out, double *
     f.E_out = h->d_E;
     {
         ProfScope ps(h, 2);
-        CU(launch_field_update(f, h->stream, field_threads(h)));
+        CU(enqueue_field(h, f));
     }
     int rc = check_status(h, "solve_poisson");
     if (rc) return rc;
@@ -886,7 +912,7 @@ int nufi_step_finish(nufi_handle *h, int64_t n, const double *partials, double *
     f.E_out = h->d_E;
     {
         ProfScope ps(h, 2);
-        CU(launch_field_update(f, h->stream, field_threads(h)));
+        CU(enqueue_field(h, f));
     }
     int rc = check_status(h, "solve_poisson");
     if (rc) return rc;
@@ -915,7 +941,7 @@ int nufi_step_finish_async(nufi_handle *h, int64_t n, const double *partials, do
     f.E_out = E_out;
     {
         ProfScope ps(h, 2);
-        CU(launch_field_update(f, h->stream, field_threads(h)));
+        CU(enqueue_field(h, f));
     }
     h->len += 1;  // provisional; nufi_check_status() reconciles with the device length
     return NUFI_OK;
@@ -1041,7 +1067,7 @@ int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, d
         if (dev[q]) base_dev[q] = user[q];
 
     static const bool nopersist = getenv("NUFI_NOPERSIST") != nullptr;
-    if (h->d == 1 && !nopersist) {
+    if (h->d == 1 && !nopersist && !h->large) {
         // whole run in one cooperative launch (run_1d.cu)
         Run1DParams P{};
         P.tp = trace_params(h, 0, 0);
@@ -1142,7 +1168,7 @@ int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, d
     }
     int rc = check_status(h, "solve_poisson");  // synchronises
     if (rc) return rc;
-    if (h->mg_world > 1 && h->d == 1 && !nopersist) {
+    if (h->mg_world > 1 && h->d == 1 && !nopersist && !h->large) {
         int err = 0;
         CU(cudaMemcpy(&err, h->mg_error, sizeof(int), cudaMemcpyDeviceToHost));
         if (err) return fail(NUFI_ERR_COMM, "multi-rank run: a peer rank did not arrive within 4 s (watchdog)");
@@ -1257,7 +1283,10 @@ int nufi_moments(nufi_handle *h, int64_t n, double *out, int64_t *evals) {
     const double measure = std::pow(h->hx, (double)h->d) * h->hv_d;  // density.py:107
     {
         ProfScope ps(h, 0, point_steps(h, n > 0 ? n + 1 : 0, h->b_hi - h->b_lo));
-        CU(launch_sweep_moments(h->d, ppt, h->pow2, p, h->K, ctas_s, threads, h->stream));
+        if (h->gl)
+            CU(launch_trace_rho_global(h->d, true, h->pow2, p, h->K, ctas_s, threads, h->stream));
+        else
+            CU(launch_sweep_moments(h->d, ppt, h->pow2, p, h->K, ctas_s, threads, h->stream));
     }
     CU(launch_reduce_moments(h->mom_part, ctas_s, h->d, measure, h->d_mom, h->stream));
     CU(cudaMemcpyAsync(out, h->d_mom, nm * sizeof(double), cudaMemcpyDefault, h->stream));

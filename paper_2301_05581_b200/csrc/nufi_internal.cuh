@@ -26,7 +26,8 @@ constexpr int MAX_D = 3;
 #ifndef NUFI_BARRIER_SLEEP_NS
 #define NUFI_BARRIER_SLEEP_NS 32
 #endif
-constexpr int MAX_FIELD_NODES = 4096;  // single-CTA field update limit (Nx^d)
+constexpr int MAX_FIELD_NODES = 4096;  // single-CTA field update limit (Nx^d); beyond: field_large.cu
+constexpr int MAX_GRID_NODES = 1 << 21;  // supported Nx^d (128^3)
 
 // ----------------------------------------------------------------------------
 // f0 descriptor (initial.py:25-56, 165-180)

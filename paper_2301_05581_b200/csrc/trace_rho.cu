@@ -29,7 +29,9 @@ namespace nufi {
 // half kick through slab n, kernels.py:194-196), f = f0(foot), and per-CTA sums
 // of f, f^2, f ln f, |v|^2 f / 2, v_a f at the UNTRACED quadrature point plus
 // (f_min, f_max) -> p.partial[cta][mom_count(D)].
-template <int D, int PPT, bool POW2, int NX, bool MOM>
+// GL = true: slabs too large for a shared-memory ring (large grids) are read in place
+// from the (L2-resident where it fits) global history instead of being staged.
+template <int D, int PPT, bool POW2, int NX, bool MOM, bool GL = false>
 __global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams p, const double K) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int warps = blockDim.x >> 5;
@@ -41,7 +43,7 @@ __global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams 
     const int slab_elems = p.ev_slab_elems;
 
     double *ring = reinterpret_cast<double *>(smem_raw);
-    uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)stages * sps * slab_elems);
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + (GL ? 0 : (size_t)stages * sps * slab_elems));
     uint64_t *empty = full + stages;
     double *red = ring;  // 3 * blockDim.x, aliases the ring once every stage is consumed
 
@@ -76,16 +78,18 @@ __global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams 
         tma_bulk_g2s(ring + (size_t)s * sps * slab_elems, p.ev_hist + (size_t)k_lo * slab_elems, bytes, &full[s]);
     };
 
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < stages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], warps);
+    if (!GL) {
+        if (threadIdx.x == 0) {
+            for (int s = 0; s < stages; ++s) {
+                mbar_init(&full[s], 1);
+                mbar_init(&empty[s], warps);
+            }
+            fence_mbar_init();
         }
-        fence_mbar_init();
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int it = 0; it < min(stages, total_it); ++it) issue(it);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int it = 0; it < min(stages, total_it); ++it) issue(it);
+        }
     }
 
     double acc = 0.0, fmn = DBL_MAX, fmx = -DBL_MAX;
@@ -120,19 +124,21 @@ __global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams 
             const uint32_t u = (uint32_t)(it / stages);
             const int k_hi = n - 1 - st * sps;
             const int k_lo = max(0, k_hi - sps + 1);
-            mbar_wait(&full[s], u & 1u);
-            const double *buf = ring + (size_t)s * sps * slab_elems;
+            if (!GL) mbar_wait(&full[s], u & 1u);
+            const double *buf = GL ? p.ev_hist + (size_t)k_lo * slab_elems : ring + (size_t)s * sps * slab_elems;
             // slab 0 is stored pre-halved (field_common.cuh), so every kick is uniform
             for (int k = k_hi; k >= k_lo; --k) {
                 const double *slab = buf + (size_t)(k - k_lo) * slab_elems;
 #pragma unroll
                 for (int pp = 0; pp < PPT; ++pp) substep<D, POW2, NX>(X[pp], V[pp], slab, N, K, false);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
-            if (threadIdx.x == 0 && it + stages < total_it) {
-                mbar_wait(&empty[s], u & 1u);
-                issue(it + stages);
+            if (!GL) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+                if (threadIdx.x == 0 && it + stages < total_it) {
+                    mbar_wait(&empty[s], u & 1u);
+                    issue(it + stages);
+                }
             }
         }
 
@@ -301,14 +307,33 @@ size_t trace_rho_smem_bytes(const TraceRhoParams &p, int threads) {
     return (ring > red ? ring : red) + 2 * p.stages * sizeof(uint64_t);
 }
 
-template <int D, int PPT, bool POW2, int NX, bool MOM = false>
+template <int D, int PPT, bool POW2, int NX, bool MOM = false, bool GL = false>
 static cudaError_t launch_one(const TraceRhoParams &p, double K, int ctas, int threads, size_t smem,
                               cudaStream_t st) {
-    auto kern = trace_rho_kernel<D, PPT, POW2, NX, MOM>;
+    auto kern = trace_rho_kernel<D, PPT, POW2, NX, MOM, GL>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<ctas, threads, smem, st>>>(p, K);
     return cudaGetLastError();
+}
+
+// large grids: slabs read in place from global memory (no ring), one point per thread
+cudaError_t launch_trace_rho_global(int d, bool mom, bool pow2, const TraceRhoParams &p, double K, int ctas,
+                                    int threads, cudaStream_t st) {
+    const size_t smem = (size_t)(mom_sums(3) + 2) * (size_t)threads * sizeof(double) + 64;
+#define NUFI_GL(DD)                                                                                           \
+    if (d == DD) {                                                                                            \
+        if (mom)                                                                                              \
+            return pow2 ? launch_one<DD, 1, true, 0, true, true>(p, K, ctas, threads, smem, st)             \
+                        : launch_one<DD, 1, false, 0, true, true>(p, K, ctas, threads, smem, st);           \
+        return pow2 ? launch_one<DD, 1, true, 0, false, true>(p, K, ctas, threads, smem, st)                \
+                    : launch_one<DD, 1, false, 0, false, true>(p, K, ctas, threads, smem, st);              \
+    }
+    NUFI_GL(1)
+    NUFI_GL(2)
+    NUFI_GL(3)
+#undef NUFI_GL
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_trace_rho(int d, int ppt, bool pow2, const TraceRhoParams &p, double K, int ctas, int threads,

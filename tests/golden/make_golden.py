@@ -56,6 +56,11 @@ CONFIGS = {
     "rag1": dict(d=1, Nx=24, Nv=40, vmax=6.0, tau=1 / 8, N=40, bench="weak_landau_1d", alpha=0.05, keep=41),
     "rag2": dict(d=2, Nx=6, Nv=10, vmax=6.0, tau=1 / 8, N=16, bench="strong_landau_2d", alpha=0.3, keep=17),
     "rag3": dict(d=3, Nx=5, Nv=3, vmax=5.0, tau=1 / 8, N=8, bench="weak_landau_3d", alpha=0.05, keep=9),
+    # grids beyond one CTA (Nx^d > 4096: multi-CTA tail; slabs > 100 KB: in-place trace)
+    "big1": dict(d=1, Nx=5000, Nv=16, vmax=6.0, tau=1 / 8, N=6, bench="weak_landau_1d", alpha=0.05, keep=7),
+    "big2": dict(d=2, Nx=72, Nv=6, vmax=6.0, tau=1 / 8, N=6, bench="strong_landau_2d", alpha=0.2, keep=7),
+    "big2g": dict(d=2, Nx=120, Nv=4, vmax=6.0, tau=1 / 8, N=4, bench="strong_landau_2d", alpha=0.2, keep=5),
+    "big3": dict(d=3, Nx=22, Nv=3, vmax=5.0, tau=1 / 8, N=4, bench="weak_landau_3d", alpha=0.05, keep=5),
     # FP32 history mode (PotentialHistory(dtype=float32), spline.py:118-125)
     "kat_wl_f32": dict(d=1, Nx=32, Nv=128, vmax=10.0, tau=1 / 16, N=160, bench="weak_landau_1d", alpha=None,
                        keep=161, dtype="float32"),
@@ -65,7 +70,7 @@ CONFIGS = {
 
 
 # history length used for the trace goldens
-TRACE_N = {"kat_wl": 40, "tiny2": 20, "tiny3": 12, "wl3r": 16, "rag1": 30, "rag2": 12, "rag3": 7}
+TRACE_N = {"kat_wl": 40, "tiny2": 20, "tiny3": 12, "wl3r": 16, "rag1": 30, "rag2": 12, "rag3": 7, "big3": 3}
 
 
 def build(cfg):

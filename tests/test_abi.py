@@ -103,22 +103,18 @@ def test_validation_errors_without_gpu():
 
 
 def test_size_limits_without_gpu():
-    """Maximum sizes: the single-CTA field update takes Nx^d <= 4096 (every BASELINE grid;
-    wl3 = 16^3 is exactly the limit); larger grids are refused with ConfigError before any
-    device work, as are unknown flags and v_blocks that do not divide Nv^d."""
+    """Maximum sizes: grids up to Nx^d = 2^21 (128^3) are accepted (beyond 4096 nodes the
+    tail runs multi-CTA, field_large.cu); larger grids are refused with ConfigError before
+    any device work, as are unknown flags."""
     from paper_2301_05581_b200.configs import workload
     from paper_2301_05581_b200.errors import ConfigError, UsageError
 
     w = workload("wl3")
     cfg = _lib.make_config(w.grid, w.ic, w.tau, 10)
-    cfg.Nx = 17  # 4913 nodes
-    with pytest.raises(ConfigError, match="single-CTA field update limit"):
+    cfg.Nx = 129  # 2 146 689 nodes
+    with pytest.raises(ConfigError, match="supported grid size"):
         _lib.Handle(cfg, 0)
     w2 = workload("wl2")
-    cfg = _lib.make_config(w2.grid, w2.ic, w2.tau, 10)
-    cfg.Nx = 65  # 4225 nodes
-    with pytest.raises(ConfigError):
-        _lib.Handle(cfg, 0)
     cfg = _lib.make_config(w2.grid, w2.ic, w2.tau, 10)
     cfg.flags = 8
     with pytest.raises(UsageError, match="flags"):

@@ -36,7 +36,7 @@ def _hist_from(name, coeffs, n_rows):
 # trace_backward: bit-exact parity mode, fast mode within tolerance
 # ---------------------------------------------------------------------------
 
-@pytest.mark.parametrize("name", ["kat_wl", "tiny2", "tiny3", "wl3r", "rag1", "rag2", "rag3"])
+@pytest.mark.parametrize("name", ["kat_wl", "tiny2", "tiny3", "wl3r", "rag1", "rag2", "rag3", "big3"])
 @pytest.mark.parametrize("hk", [0, 1])
 def test_trace_parity_bit_exact(name, hk):
     t = golden(f"trace_{name}")
@@ -51,7 +51,7 @@ def test_trace_parity_bit_exact(name, hk):
     assert np.array_equal(V, t[f"V{hk}"]), np.abs(V - t[f"V{hk}"]).max()
 
 
-@pytest.mark.parametrize("name", ["kat_wl", "tiny2", "tiny3", "wl3r", "rag1", "rag2", "rag3"])
+@pytest.mark.parametrize("name", ["kat_wl", "tiny2", "tiny3", "wl3r", "rag1", "rag2", "rag3", "big3"])
 @pytest.mark.parametrize("hk", [0, 1])
 def test_trace_fast_close(name, hk):
     t = golden(f"trace_{name}")
@@ -94,7 +94,7 @@ def test_trace_errors_and_edge_cases():
 # compute_rho drop-in and the field update on golden histories
 # ---------------------------------------------------------------------------
 
-@pytest.mark.parametrize("name", ["kat_wl", "tiny2", "tiny3", "wl1", "rag1", "rag2", "rag3"])
+@pytest.mark.parametrize("name", ["kat_wl", "tiny2", "tiny3", "wl1", "rag1", "rag2", "rag3", "big1", "big2g", "big3"])
 def test_compute_rho_on_reference_history(name):
     g = golden(name)
     keep = g["rho"].shape[0]
@@ -120,7 +120,7 @@ def test_compute_rho_requires_history():
     assert ctx.field_evals == 0 and r.density.values.shape == (32,)
 
 
-@pytest.mark.parametrize("name", ["kat_wl", "tiny2", "tiny3", "rag1", "rag2", "rag3"])
+@pytest.mark.parametrize("name", ["kat_wl", "tiny2", "tiny3", "rag1", "rag2", "rag3", "big1", "big2", "big3"])
 def test_advance_matches_solve_fit_append(name):
     """solve_poisson + fit_spline + append + electric_energy + E from the reference's rho."""
     g = golden(name)
@@ -172,7 +172,8 @@ def _check_run(name, g, sim, res, w_until=None, rho_tol=RHO_TOL):
     return relW
 
 
-@pytest.mark.parametrize("name", ["kat_wl", "tiny2", "tiny3", "wl1", "rag1", "rag2", "rag3"])
+@pytest.mark.parametrize("name", ["kat_wl", "tiny2", "tiny3", "wl1", "rag1", "rag2", "rag3", "big1", "big2", "big2g",
+                                  "big3"])
 def test_run_vs_reference(name):
     g = golden(name)
     N = len(g["W"]) - 1

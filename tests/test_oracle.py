@@ -15,8 +15,9 @@ import pytest
 from oracle import oracle as O
 from tests._util import golden, normwise
 
-TRACE_CASES = ["kat_wl", "tiny2", "tiny3", "wl3r", "rag1", "rag2", "rag3"]
-LOOP_CASES = ["kat_wl", "eq1", "tiny2", "tiny3", "wl1", "kat_wl_f32", "tiny2_f32", "rag1", "rag2", "rag3"]
+TRACE_CASES = ["kat_wl", "tiny2", "tiny3", "wl3r", "rag1", "rag2", "rag3", "big3"]
+LOOP_CASES = ["kat_wl", "eq1", "tiny2", "tiny3", "wl1", "kat_wl_f32", "tiny2_f32", "rag1", "rag2", "rag3", "big1",
+              "big2", "big2g", "big3"]
 
 
 @pytest.fixture(scope="module", autouse=True)
