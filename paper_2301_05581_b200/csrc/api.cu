@@ -975,7 +975,8 @@ static unsigned *mg_flags(const nufi_handle *h, void *buf) {
 
 int nufi_mg_setup(nufi_handle *h, int world, int rank, int emulate, void *ipc_handle_out) {
     CHECK_HANDLE(h);
-    if (h->d != 1) return fail(NUFI_ERR_USAGE, "the fused multi-rank run is the d = 1 persistent kernel");
+    if (h->d != 1 || h->large)
+        return fail(NUFI_ERR_USAGE, "the fused multi-rank run is the d = 1 persistent kernel (Nx <= 4096)");
     if (world < 2 || world > NUFI_MG_MAX || rank < 0 || rank >= world)
         return fail(NUFI_ERR_USAGE, "world must be 2..8 and 0 <= rank < world");
     if (h->B % world) return fail(NUFI_ERR_USAGE, "v_blocks must be a multiple of the rank count");
