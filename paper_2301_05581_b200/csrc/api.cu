@@ -1068,7 +1068,8 @@ int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, d
         if (dev[q]) base_dev[q] = user[q];
 
     static const bool nopersist = getenv("NUFI_NOPERSIST") != nullptr;
-    if (h->d == 1 && !nopersist && !h->large) {
+    bool persist = h->d == 1 && !nopersist && !h->large;
+    if (persist) {
         // whole run in one cooperative launch (run_1d.cu)
         Run1DParams P{};
         P.tp = trace_params(h, 0, 0);
@@ -1118,7 +1119,15 @@ int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, d
             const double ps = (double)h->nodes * h->V * (double)((n_last * (n_last + 1) - (first - 1) * first) / 2);
             ProfScope prof(h, 0, ps);
             int grid = 0;
-            CU(launch_run_1d(P, h->threads + 32, h->device, h->stream, &grid));
+            const cudaError_t le = launch_run_1d(P, h->threads + 32, h->device, h->stream, &grid);
+            if (le == cudaErrorCooperativeLaunchTooLarge && h->mg_world == 1) {
+                // the device cannot host the whole grid at once (e.g. shared with other
+                // work): fall back to one launch per step, same results
+                cudaGetLastError();
+                persist = false;
+            } else {
+                CU(le);
+            }
         }
         if (stamps) {
             std::vector<unsigned long long> st(3 * steps + 10 + 6 * 1024);
@@ -1147,10 +1156,11 @@ int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, d
             }
         }
         for (int q = 0; q < 4; ++q)
-            if (user[q] && !dev[q])
+            if (persist && user[q] && !dev[q])
                 CU(cudaMemcpyAsync(base_host[q], base_dev[q], steps * width[q] * sizeof(double),
                                    cudaMemcpyDeviceToHost, h->stream));
-    } else {
+    }
+    if (!persist) {
     for (int64_t n = first; n <= n_last; ++n) {
         const int64_t row = n - first;
         StepOut o;
@@ -1169,7 +1179,7 @@ int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, d
     }
     int rc = check_status(h, "solve_poisson");  // synchronises
     if (rc) return rc;
-    if (h->mg_world > 1 && h->d == 1 && !nopersist && !h->large) {
+    if (h->mg_world > 1 && persist) {
         int err = 0;
         CU(cudaMemcpy(&err, h->mg_error, sizeof(int), cudaMemcpyDeviceToHost));
         if (err) return fail(NUFI_ERR_COMM, "multi-rank run: a peer rank did not arrive within 4 s (watchdog)");
