@@ -42,6 +42,7 @@ cudaError_t launch_trace_rho_global(int d, bool mom, bool pow2, const TraceRhoPa
                                     int threads, cudaStream_t st);
 cudaError_t launch_field_large(const FieldParams &f, double *scratch, cudaStream_t st);
 size_t field_large_scratch_doubles(int nodes);
+cudaError_t launch_halo_table(int d, int N, int *halo, cudaStream_t st);
 cudaError_t launch_field_tables(double *tw, double *fac, double *k2, int d, int N, int nodes, double k_scale,
                                 cudaStream_t st);
 cudaError_t launch_run_1d(const Run1DParams &P, int threads, int device, cudaStream_t st, int *grid_out);
@@ -130,6 +131,7 @@ struct nufi_handle {
     bool large = false;   // Nx^d > MAX_FIELD_NODES: multi-CTA tail (field_large.cu)
     bool gl = false;      // slabs too large for a shared-memory ring: traced in place (GL kernels)
     double *large_scratch = nullptr;
+    int *halo = nullptr;  // d >= 2 evaluation-slab source indices
     int f32 = 0;      // NUFI_FLAG_F32_HISTORY
 
     // optional per-launch event timing (nufi_profile)
@@ -511,6 +513,10 @@ int nufi_create(const nufi_config *cfg, int device, void *stream, nufi_handle **
     CU(dalloc(&h->d_status, sizeof(int), h->stream));
     CU(dalloc(&h->d_len, sizeof(int64_t), h->stream));
     if (h->large) CU(dalloc(&h->large_scratch, field_large_scratch_doubles(h->nodes) * sizeof(double), h->stream));
+    if (c.d >= 2) {
+        CU(dalloc(&h->halo, (size_t)ev_slab_raw_elems(c.d, c.Nx) * sizeof(int), h->stream));
+        CU(launch_halo_table(c.d, c.Nx, h->halo, h->stream));
+    }
     CU(dalloc(&h->tables, (4 * (size_t)h->N + 3 * nodes) * sizeof(double), h->stream));
     CU(dalloc(&h->ticket, sizeof(unsigned), h->stream));
     CU(dalloc(&h->barrier, sizeof(unsigned), h->stream));
@@ -537,7 +543,7 @@ int nufi_destroy(nufi_handle *h) {
                     (void *)h->d_rho, (void *)h->d_E, (void *)h->d_W, (void *)h->d_stats, (void *)h->d_rho_bar,
                     (void *)h->d_status, (void *)h->d_len, (void *)h->run_dev, (void *)h->tables,
                     (void *)h->ticket, (void *)h->barrier, (void *)h->mom_part, (void *)h->d_mom,
-                    (void *)h->large_scratch})
+                    (void *)h->large_scratch, (void *)h->halo})
         if (p) cudaFreeAsync(p, h->stream);
     for (int q = 0; q < NUFI_MG_MAX; ++q) {
         if (h->mg_opened[q]) cudaIpcCloseMemHandle(h->mg_peer[q]);
@@ -663,9 +669,26 @@ static FieldParams field_params(nufi_handle *h);
 
 // the step tail: one CTA (field_update_body) or, beyond MAX_FIELD_NODES, the multi-CTA
 // sequence of field_large.cu
-static cudaError_t enqueue_field(nufi_handle *h, const FieldParams &f) {
-    if (h->large) return launch_field_large(f, h->large_scratch, h->stream);
-    return launch_field_update(f, h->stream, field_threads(h));
+static cudaError_t enqueue_field(nufi_handle *h, const FieldParams &f_in) {
+    if (h->large) return launch_field_large(f_in, h->large_scratch, h->stream);
+    static const char *dbg = getenv("NUFI_FIELD_STAMPS");  // debug: phase timestamps of the tail
+    if (!dbg) return launch_field_update(f_in, h->stream, field_threads(h));
+    FieldParams f = f_in;
+    unsigned long long *ts = nullptr, host[10] = {0};
+    cudaMalloc(&ts, sizeof host);
+    cudaMemsetAsync(ts, 0, sizeof host, h->stream);
+    f.tstamps = ts;
+    cudaError_t e = launch_field_update(f, h->stream, field_threads(h));
+    cudaMemcpyAsync(host, ts, sizeof host, cudaMemcpyDeviceToHost, h->stream);
+    cudaStreamSynchronize(h->stream);
+    cudaFree(ts);
+    if (FILE *fp = fopen(dbg, "a")) {
+        for (int k = 1; k < 10; ++k)
+            if (host[k]) fprintf(fp, " %d:%.2f", k, (double)(host[k] - host[0]) * 1e-3);
+        fprintf(fp, "\n");
+        fclose(fp);
+    }
+    return e;
 }
 
 static FieldParams field_params(nufi_handle *h) {
@@ -688,6 +711,7 @@ static FieldParams field_params(nufi_handle *h) {
         f.gc = f.k2 + h->nodes;
         f.gp = f.gc + h->N;
     }
+    f.halo = h->halo;
     f.hist = h->hist;
     f.ev_hist = h->ev_hist;
     f.ev_slab_elems = h->ev_elems;

@@ -38,6 +38,8 @@ struct FieldParams {
     // d = 1 only: circulant kernels of the (linear, translation-invariant) field
     // map, c = gc (*) rho and phi = gp (*) rho (field_conv_kernels_kernel)
     const double *gc, *gp;
+    // d >= 2: source index of every evaluation-slab element (ev_halo_source, tabulated)
+    const int *halo;
     // v-sums: B blocks of rows_per_block rows of Nx^d sums, combined in fixed order;
     // min / max: B blocks of mm_per_block (min, max) pairs
     const double *sums;
@@ -99,7 +101,7 @@ struct Run1DParams {
 // shared-memory doubles the routine needs: 4 work arrays, twiddles, the
 // per-block sums (B <= 8 blocks staged when rows_per_block > 1), scratch
 __host__ __device__ constexpr int field_smem_doubles(int nodes, int N, bool staged) {
-    return 4 * nodes + 2 * N + (staged ? 8 * nodes : 0) + 64;
+    return 4 * nodes + 2 * N + (staged ? 8 * nodes : 0) + 128;  // scratch: 3 x 32 warp slots (cta_sum_min_max)
 }
 
 // FP32 history mode: a stored coefficient is the float32 rounding of the fit
@@ -138,6 +140,36 @@ __device__ __forceinline__ double cta_max(double v, double *scratch) {
     return s;
 }
 
+// sum, min and max over the CTA with one shared-memory round trip (the sum in the
+// order of cta_sum: warp xor-tree, then warps in order); every thread gets the results
+__device__ __forceinline__ void cta_sum_min_max(double s, double mn, double mx, double *scratch, double &S,
+                                                double &MN, double &MX) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    s = warp_sum(s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    __syncthreads();
+    if (lane == 0) {
+        scratch[warp] = s;
+        scratch[32 + warp] = mn;
+        scratch[64 + warp] = mx;
+    }
+    __syncthreads();
+    double a = 0.0, b = DBL_MAX, c = -DBL_MAX;
+    for (int w = 0; w < nw; ++w) {
+        a += scratch[w];
+        b = fmin(b, scratch[32 + w]);
+        c = fmax(c, scratch[64 + w]);
+    }
+    __syncthreads();
+    S = a;
+    MN = b;
+    MX = c;
+}
+
 // One separable DFT pass along the axis of stride st:
 //   out[e] = sum_x in[e with x on the axis] * exp(sign * 2 pi i alpha x / N)
 // Each output is summed by G consecutive lanes (G | 32), combined by shuffles.
@@ -173,6 +205,51 @@ __device__ __forceinline__ void dft_pass(const double *__restrict__ ire, const d
         }
     }
     __syncthreads();
+}
+
+// One separable radix-2 FFT pass along the axis of stride st (N = 2^logN): the same
+// transform as dft_pass -- out[.. alpha ..] = sum_x in[.. x ..] e^{sign 2 pi i alpha x / N}
+// -- in N log N: a bit-reversed copy along the axis into (ore, oim), then log2 N in-place
+// butterfly stages (decimation in time), a CTA barrier after each.
+__device__ __forceinline__ void fft_axis_pass(const double *__restrict__ ire, const double *__restrict__ iim,
+                                              double *__restrict__ ore, double *__restrict__ oim,
+                                              const double *__restrict__ twc, const double *__restrict__ tws,
+                                              int N, int logN, int nodes, int st, double sign) {
+    // N and st are powers of two here: every index split is a shift or a mask
+    const int T = blockDim.x;
+    const int logst = 31 - __clz(st);
+    for (int e = threadIdx.x; e < nodes; e += T) {
+        const int x = (e >> logst) & (N - 1);
+        const int rx = (int)(__brev((unsigned)x) >> (32 - logN));
+        const int dst = e + ((rx - x) << logst);
+        ore[dst] = ire[e];
+        oim[dst] = iim[e];
+    }
+    __syncthreads();
+    for (int lh = 0; lh < logN; ++lh) {
+        const int h = 1 << lh;
+        const int tws_shift = logN - 1 - lh;  // twiddle index pos * N / (2h)
+        const int loglines = 31 - __clz(nodes) - logN;  // lines = nodes / N
+        for (int b = threadIdx.x; b < (nodes >> 1); b += T) {
+            // consecutive lanes: along the line for the contiguous axis (st = 1), across
+            // lines otherwise -- either way neighbouring lanes touch neighbouring banks
+            const int line = st == 1 ? b >> (logN - 1) : b & ((1 << loglines) - 1);
+            const int j = st == 1 ? b & ((N >> 1) - 1) : b >> loglines;
+            const int pos = j & (h - 1);
+            const int i0 = ((j - pos) << 1) + pos;
+            const int base = ((line >> logst) << (logst + logN)) + (line & (st - 1));
+            const int a0 = base + (i0 << logst), a1 = a0 + (h << logst);
+            const double wr = twc[pos << tws_shift], wi = sign * tws[pos << tws_shift];
+            const double ur = ore[a1], ui = oim[a1];
+            const double xr = fma(ur, wr, -ui * wi), xi = fma(ur, wi, ui * wr);
+            const double pr = ore[a0], pi = oim[a0];
+            ore[a1] = pr - xr;
+            oim[a1] = pi - xi;
+            ore[a0] = pr + xr;
+            oim[a0] = pi + xi;
+        }
+        __syncthreads();
+    }
 }
 
 // c = gc (*) r and phi = gp (*) r for small N (power of two): one output per
@@ -448,6 +525,46 @@ static __device__ __forceinline__ bool field_update_1d_body(const FieldParams &p
     return true;
 }
 
+// E at the nodes: -(N/L) sum over the 3^D f = 0 stencil (w = 1/6, 2/3, 1/6 and
+// dw = -1/2, 0, 1/2 on the differentiated axis), taps in x-slowest order, weights
+// multiplied in axis order -- the order of the former generic loop, with the
+// neighbour indices formed once per node and every loop unrolled (no local memory).
+template <int D>
+__device__ __forceinline__ void e_at_nodes(const double *c, int N, int nodes, double inv_h, double *E_out) {
+    const double w0[3] = {1.0 / 6.0, 2.0 / 3.0, 1.0 / 6.0};
+    const double dw0[3] = {-0.5, 0.0, 0.5};
+    for (int i = threadIdx.x; i < nodes; i += blockDim.x) {
+        int nb[D][3];
+        int r = i;
+#pragma unroll
+        for (int a = D - 1; a >= 0; --a) {
+            const int ia = r % N;
+            r /= N;
+            nb[a][0] = ia == 0 ? N - 1 : ia - 1;
+            nb[a][1] = ia;
+            nb[a][2] = ia == N - 1 ? 0 : ia + 1;
+        }
+#pragma unroll
+        for (int g = 0; g < D; ++g) {
+            double acc = 0.0;
+#pragma unroll
+            for (int t = 0; t < (D == 1 ? 3 : (D == 2 ? 9 : 27)); ++t) {
+                int o[3] = {t % 3, (t / 3) % 3, t / 9};
+                if (o[g] == 1) continue;  // dw = 0 at the centre tap
+                int lin = 0;
+                double w = 1.0;
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    lin = lin * N + nb[a][o[a]];
+                    w *= (a == g) ? dw0[o[a]] : w0[o[a]];
+                }
+                acc = fma(c[lin], w, acc);
+            }
+            E_out[(size_t)i * D + g] = -acc * inv_h;
+        }
+    }
+}
+
 // The whole tail.  `sm`: field_smem_doubles(nodes, N, rows_per_block > 1) doubles of shared memory
 // (B <= 8 when rows_per_block > 1).
 static __device__ __forceinline__ bool field_update_body(const FieldParams &p, double *sm) {
@@ -496,15 +613,15 @@ static __device__ __forceinline__ bool field_update_body(const FieldParams &p, d
             re1[i] = r;
             local += r;
         }
-        neut = cta_sum(local, scratch) / (double)nodes;
         double mn = DBL_MAX, mx = -DBL_MAX;
         const int mrows = p.B * p.mm_per_block;
         for (int r = threadIdx.x; r < mrows; r += T) {
             mn = fmin(mn, __ldcg(p.minmax + 2 * r));
             mx = fmax(mx, __ldcg(p.minmax + 2 * r + 1));
         }
-        fmx = cta_max(mx, scratch);
-        fmn = -cta_max(-mn, scratch);
+        double tot;
+        cta_sum_min_max(local, mn, mx, scratch, tot, fmn, fmx);
+        neut = tot / (double)nodes;
         for (int i = threadIdx.x; i < nodes; i += T) {
             re0[i] = re1[i] - neut;
             im0[i] = 0.0;
@@ -533,8 +650,10 @@ static __device__ __forceinline__ bool field_update_body(const FieldParams &p, d
             s += re0[i];
             mx = fmax(mx, fabs(re0[i]));
         }
-        const double mean = cta_sum(s, scratch) / (double)nodes;
-        const double tol = 1e-8 * cta_max(mx, scratch);
+        double tot, unused, m;
+        cta_sum_min_max(s, DBL_MAX, mx, scratch, tot, unused, m);
+        const double mean = tot / (double)nodes;
+        const double tol = 1e-8 * m;
         if (fabs(mean) > tol) {
             if (threadIdx.x == 0 && p.status) *p.status = NUFI_ERR_NUMERICAL;
             return false;  // history unchanged (the reference raises before appending)
@@ -551,7 +670,10 @@ static __device__ __forceinline__ bool field_update_body(const FieldParams &p, d
     for (int axis = d - 1; axis >= 0; --axis) {
         int st = 1;
         for (int a = axis + 1; a < d; ++a) st *= N;
-        dft_pass(ar, ai, br, bi, twc, tws, N, nodes, st, -1.0, G, pow2);
+        if (pow2)
+            fft_axis_pass(ar, ai, br, bi, twc, tws, N, 31 - __clz(N), nodes, st, -1.0);
+        else
+            dft_pass(ar, ai, br, bi, twc, tws, N, nodes, st, -1.0, G, pow2);
         double *tr = ar, *ti = ai;
         ar = br, ai = bi, br = tr, bi = ti;
     }
@@ -577,7 +699,10 @@ static __device__ __forceinline__ bool field_update_body(const FieldParams &p, d
     for (int axis = d - 1; axis >= 0; --axis) {
         int st = 1;
         for (int a = axis + 1; a < d; ++a) st *= N;
-        dft_pass(ar, ai, br, bi, twc, tws, N, nodes, st, 1.0, G, pow2);
+        if (pow2)
+            fft_axis_pass(ar, ai, br, bi, twc, tws, N, 31 - __clz(N), nodes, st, 1.0);
+        else
+            dft_pass(ar, ai, br, bi, twc, tws, N, nodes, st, 1.0, G, pow2);
         double *tr = ar, *ti = ai;
         ar = br, ai = bi, br = tr, bi = ti;
     }
@@ -614,7 +739,8 @@ static __device__ __forceinline__ bool field_update_body(const FieldParams &p, d
         }
     } else {
         const int raw = ev_slab_raw_elems(d, N);
-        for (int e = threadIdx.x; e < raw; e += T) put(e, evs * hist_round(c[ev_halo_source(d, N, e)], p.f32_hist));
+        for (int e = threadIdx.x; e < raw; e += T)
+            put(e, evs * hist_round(c[p.halo ? p.halo[e] : ev_halo_source(d, N, e)], p.f32_hist));
     }
     for (int e = ev_slab_raw_elems(d, N) + threadIdx.x; e < p.ev_slab_elems; e += T) put(e, 0.0);
     if (threadIdx.x == 0 && p.hist_len) *p.hist_len = p.slot + 1;
@@ -622,32 +748,12 @@ static __device__ __forceinline__ bool field_update_body(const FieldParams &p, d
     NUFI_STAMP(p, 7);
     // ---- E at the nodes: -grad of the spline at x_i (f = 0 stencil (1/6, 2/3, 1/6) / (-1/2, 0, 1/2)) ----
     if (p.E_out) {
-        const double w0[3] = {1.0 / 6.0, 2.0 / 3.0, 1.0 / 6.0};
-        const double dw0[3] = {-0.5, 0.0, 0.5};
-        for (int i = threadIdx.x; i < nodes; i += T) {
-            int idx[3] = {0, 0, 0};
-            int r = i;
-            for (int a = d - 1; a >= 0; --a) {
-                idx[a] = r % N;
-                r /= N;
-            }
-            const int taps = d == 1 ? 3 : (d == 2 ? 9 : 27);
-            for (int g = 0; g < d; ++g) {
-                double acc = 0.0;
-                for (int t = 0; t < taps; ++t) {
-                    const int o[3] = {t % 3, (t / 3) % 3, t / 9};
-                    if (o[g] == 1) continue;  // dw = 0 at the centre tap
-                    int lin = 0;
-                    double w = 1.0;
-                    for (int a = 0; a < d; ++a) {
-                        lin = lin * N + (idx[a] + o[a] - 1 + N) % N;
-                        w *= (a == g) ? dw0[o[a]] : w0[o[a]];
-                    }
-                    acc = fma(c[lin], w, acc);
-                }
-                p.E_out[(size_t)i * d + g] = -acc * p.inv_h;
-            }
-        }
+        if (d == 2)
+            e_at_nodes<2>(c, N, nodes, p.inv_h, p.E_out);
+        else if (d == 3)
+            e_at_nodes<3>(c, N, nodes, p.inv_h, p.E_out);
+        else
+            e_at_nodes<1>(c, N, nodes, p.inv_h, p.E_out);
     }
     NUFI_STAMP(p, 8);
     return true;

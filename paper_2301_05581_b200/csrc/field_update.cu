@@ -182,6 +182,18 @@ cudaError_t launch_field_tables(double *tw, double *fac, double *k2, int d, int 
     return cudaGetLastError();
 }
 
+// d >= 2: the halo source index of every evaluation-slab element, once per handle
+__global__ void halo_table_kernel(int d, int N, int raw, int *halo) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < raw; e += gridDim.x * blockDim.x)
+        halo[e] = ev_halo_source(d, N, e);
+}
+
+cudaError_t launch_halo_table(int d, int N, int *halo, cudaStream_t st) {
+    const int raw = ev_slab_raw_elems(d, N);
+    halo_table_kernel<<<(raw + 255) / 256 < 1024 ? (raw + 255) / 256 : 1024, 256, 0, st>>>(d, N, raw, halo);
+    return cudaGetLastError();
+}
+
 // Evaluation slabs (trace_common.cuh layouts) for raw rows [r0, r1) of hist.
 // f32: FP32 history mode -- round the raw row in place first (spline.py:118-125, 140).
 __global__ void build_ev_slabs_kernel(double *__restrict__ hist, double *__restrict__ ev_hist, int d, int N,
