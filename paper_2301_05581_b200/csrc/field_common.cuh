@@ -500,14 +500,14 @@ static __device__ __forceinline__ bool field_update_1d_body(const FieldParams &p
         const double K = evs * p.K;
         const double A = K * ((g0 + 0.5 * g1) + 0.25 * g2), Bc = K * (g1 + g2), C = K * g2;
         if (evg) {
-            evg[i] = A;
-            evg[N + i] = Bc;
-            evg[2 * N + i] = C;
+            evg[d1_ia(i, N)] = A;
+            evg[d1_ib(i, N)] = Bc;
+            evg[d1_ic(i, N)] = C;
         }
         if (evl) {
-            evl[i] = A;
-            evl[N + i] = Bc;
-            evl[2 * N + i] = C;
+            evl[d1_ia(i, N)] = A;
+            evl[d1_ib(i, N)] = Bc;
+            evl[d1_ic(i, N)] = C;
         }
         if (hrow) hrow[i] = c1;
         if (p.coeffs_out) p.coeffs_out[i] = c1;
@@ -733,9 +733,9 @@ static __device__ __forceinline__ bool field_update_body(const FieldParams &p, d
             const double g1 = (c0 - 2.0 * c1) + c2;
             const double g2 = (1.5 * (c1 - c2)) + 0.5 * (c3 - c0);
             const double K = evs * p.K;
-            put(i, K * ((g0 + 0.5 * g1) + 0.25 * g2));
-            put(N + i, K * (g1 + g2));
-            put(2 * N + i, K * g2);
+            put(d1_ia(i, N), K * ((g0 + 0.5 * g1) + 0.25 * g2));
+            put(d1_ib(i, N), K * (g1 + g2));
+            put(d1_ic(i, N), K * g2);
         }
     } else {
         const int raw = ev_slab_raw_elems(d, N);

@@ -196,9 +196,9 @@ __global__ void large_append_kernel(LargeParams P, const double *c) {
                 const double g1 = (c0 - 2.0 * c1) + c2;
                 const double g2 = (1.5 * (c1 - c2)) + 0.5 * (c3 - c0);
                 const double K = evs * p.K;
-                evg[i] = K * ((g0 + 0.5 * g1) + 0.25 * g2);
-                evg[N + i] = K * (g1 + g2);
-                evg[2 * N + i] = K * g2;
+                evg[d1_ia(i, N)] = K * ((g0 + 0.5 * g1) + 0.25 * g2);
+                evg[d1_ib(i, N)] = K * (g1 + g2);
+                evg[d1_ic(i, N)] = K * g2;
             }
         } else {
             const int raw = ev_slab_raw_elems(d, N);

@@ -213,9 +213,9 @@ __global__ void build_ev_slabs_kernel(double *__restrict__ hist, double *__restr
             const double g0 = 0.5 * (c2 - c0);
             const double g1 = (c0 - 2.0 * c1) + c2;
             const double g2 = (1.5 * (c1 - c2)) + 0.5 * (c3 - c0);
-            ev[i] = K * ((g0 + 0.5 * g1) + 0.25 * g2);
-            ev[N + i] = K * (g1 + g2);
-            ev[2 * N + i] = K * g2;
+            ev[d1_ia(i, N)] = K * ((g0 + 0.5 * g1) + 0.25 * g2);
+            ev[d1_ib(i, N)] = K * (g1 + g2);
+            ev[d1_ic(i, N)] = K * g2;
         }
     } else {
         const int raw = ev_slab_raw_elems(d, N);

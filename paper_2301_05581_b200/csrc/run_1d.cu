@@ -41,12 +41,10 @@ template <int NX>
 __device__ __forceinline__ void kick1(double &X, double &V, const double *__restrict__ slab, int N) {
     const double s = X + MAGIC;
     const int n_ = NX ? NX : N;
-    const char *b = reinterpret_cast<const char *>(slab);
-    const double *c = reinterpret_cast<const double *>(
-        b + (((unsigned)__double_as_longlong(s) & (unsigned)(n_ - 1)) << 3));
     const double fc = X - (s - MAGIC);
     const double XmV = X - V;
-    const double A = c[0], B = c[n_], C = c[2 * n_];
+    double A, B, C;
+    d1_fetch(slab, (int)((unsigned)__double_as_longlong(s) & (unsigned)(n_ - 1)), n_, A, B, C);
     const double t = fma(fc, C, B);
     X = fma(-fc, t, XmV - A);
     V = fma(fc, t, V + A);
@@ -55,7 +53,9 @@ __device__ __forceinline__ void kick1(double &X, double &V, const double *__rest
 __device__ __forceinline__ void kick1_any(double &X, double &V, const double *__restrict__ slab, int N) {
     double fc;
     const int i = locate_centred<false>(X, N, fc);
-    const double A = slab[i], t = fma(fc, slab[2 * N + i], slab[N + i]);
+    double A, B, C;
+    d1_fetch(slab, i, N, A, B, C);
+    const double t = fma(fc, C, B);
     const double XmV = X - V;
     X = fma(-fc, t, XmV - A);
     V = fma(fc, t, V + A);

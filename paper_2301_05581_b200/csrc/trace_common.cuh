@@ -62,6 +62,30 @@ __host__ __device__ constexpr int ev_slab_elems(int d, int N) {
     return (ev_slab_raw_elems(d, N) + 1) & ~1;
 }
 
+// d = 1 evaluation slab: three planes [A | B | C] (three 8-byte shared-memory gathers per
+// lookup).  NUFI_D1_PAIRED=1 interleaves the (A_i, B_i) pairs at 2i, 2i + 1 (one 16-byte
+// gather + one 8-byte) -- measured slower: 16-byte gathers are served per quarter warp, so
+// random cells cost more wavefronts than two 8-byte gathers (ts1 trace 76.5 -> 80.2 ms).
+#ifndef NUFI_D1_PAIRED
+#define NUFI_D1_PAIRED 0
+#endif
+__host__ __device__ constexpr int d1_ia(int i, int N) { return NUFI_D1_PAIRED ? 2 * i : i; }
+__host__ __device__ constexpr int d1_ib(int i, int N) { return NUFI_D1_PAIRED ? 2 * i + 1 : N + i; }
+__host__ __device__ constexpr int d1_ic(int i, int N) { return 2 * N + i; }
+
+__device__ __forceinline__ void d1_fetch(const double *__restrict__ slab, int i, int N, double &A, double &B,
+                                         double &C) {
+#if NUFI_D1_PAIRED
+    const double2 ab = *reinterpret_cast<const double2 *>(slab + 2 * i);
+    A = ab.x;
+    B = ab.y;
+#else
+    A = slab[i];
+    B = slab[N + i];
+#endif
+    C = slab[2 * N + i];
+}
+
 template <bool POW2>
 __device__ __forceinline__ int wrap_idx(int i, int N) {
     if (POW2) return i & (N - 1);
@@ -78,7 +102,8 @@ __device__ __forceinline__ void kick(const double (&X)[D], double (&V)[D], const
     if constexpr (D == 1) {
         double fc;
         const int i = locate_centred<POW2>(X[0], N, fc);
-        const double A = slab[i], B = slab[N + i], C = slab[2 * N + i];
+        double A, B, C;
+        d1_fetch(slab, i, N, A, B, C);
         const double kick = fma(fc, fma(fc, C, B), A);
         V[0] = half ? fma(0.5, kick, V[0]) : V[0] + kick;
         (void)K;

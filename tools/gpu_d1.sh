@@ -1,5 +1,3 @@
 set -x
 timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/d1_pytest.log 2>&1; tail -3 gpurun_out/d1_pytest.log
 for c in sl1 ts1 wl1; do timeout 300 python tools/stamps.py $c 2>&1 | grep -v "^  n=\|tail phases"; done
-NUFI_D1_PPT=1 timeout 300 python tools/stamps.py sl1 2>&1 | grep -v "^  n=\|tail phases"
-NUFI_D1_PPT=2 timeout 300 python tools/stamps.py ts1 2>&1 | grep -v "^  n=\|tail phases"
