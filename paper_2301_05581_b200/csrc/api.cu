@@ -1093,6 +1093,8 @@ int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, d
 
     static const bool nopersist = getenv("NUFI_NOPERSIST") != nullptr;
     bool persist = h->d == 1 && !nopersist && !h->large;
+    if (h->mg_world > 1 && !persist)
+        return fail(NUFI_ERR_USAGE, "a connected multi-rank handle runs only the persistent d = 1 kernel");
     if (persist) {
         // whole run in one cooperative launch (run_1d.cu)
         Run1DParams P{};

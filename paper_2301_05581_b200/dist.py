@@ -26,7 +26,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .errors import UsageError
+from .errors import NumericalConsistencyError, UsageError
 
 
 def block_range(B: int, rank: int, world: int) -> tuple[int, int]:
@@ -168,12 +168,28 @@ class DistributedSimulation:
                 outputs = dict(rho=np.empty((steps, g.n_nodes)), E=np.empty((steps, g.n_nodes, g.d)),
                                W=np.empty(steps), stats=np.empty((steps, 3)))
             ev = ctypes.c_int64(0)
-            self.history.handle.call("nufi_run", self.n_steps, _lib.ptr(outputs.get("rho")),
-                                     _lib.ptr(outputs.get("E")), _lib.ptr(outputs.get("W")),
-                                     _lib.ptr(outputs.get("stats")), ctypes.byref(ev))
-            # nufi_run counts the whole grid; this rank traced its share of the blocks
-            self.ctx.field_evals += int(ev.value) * (self.block_hi - self.block_lo) // self.B
-            return outputs
+            err = None
+            try:
+                self.history.handle.call("nufi_run", self.n_steps, _lib.ptr(outputs.get("rho")),
+                                         _lib.ptr(outputs.get("E")), _lib.ptr(outputs.get("W")),
+                                         _lib.ptr(outputs.get("stats")), ctypes.byref(ev))
+            except NumericalConsistencyError:
+                raise  # the physics, not the transport: same on every rank
+            except Exception as exc:  # a peer timed out (watchdog) or the launch failed
+                err = exc
+            # every rank agrees on the outcome before anyone trusts its history
+            flag = self.torch.tensor([0 if err is None else 1], dtype=self.torch.int32,
+                                     device=self.partials.device)
+            self.dist.all_reduce(flag, group=self.group)
+            if int(flag.item()) == 0:
+                # nufi_run counts the whole grid; this rank traced its share of the blocks
+                self.ctx.field_evals += int(ev.value) * (self.block_hi - self.block_lo) // self.B
+                return outputs
+            import warnings
+
+            warnings.warn(f"fused multi-rank run failed ({err or 'on a peer'}); rerunning with the per-step NCCL loop")
+            self.fused = False
+            self.history.truncate(first)
         host = outputs is None
         if host:
             g = self.grid
