@@ -60,6 +60,9 @@ struct FieldParams {
     int finish_only;    // compute_rho only: stop after rho / stats
     int f32_hist;       // FP32 history (spline.py:118-125): stored slabs rounded to float
     unsigned long long *tstamps;  // debug: phase timestamps (thread 0), 10 slots
+    // d = 1: shared-memory doubles available beyond field_smem_doubles(N, N, true) for staging
+    // the tile-row partials with cp.async (0: read them with register loads)
+    int64_t stage_cap;
 };
 
 #define NUFI_MG_MAX 8
@@ -304,17 +307,84 @@ static __device__ __forceinline__ void fft_radix2(double *re, double *im, const 
     }
 }
 
+// Skewed shared-memory layouts of the d = 1 convolution operands (N <= 64), so the
+// blocked loads of circulant_blocked hit distinct banks: r at i + i/8, kernels at m + m/4.
+__device__ __forceinline__ int rsk(int i) { return i + (i >> 3); }
+__device__ __forceinline__ int gsk(int m) { return m + (m >> 2); }
+
+// c = gc (*) r and phi = gp (*) r for 4 <= N <= 64 (power of two), operands skewed
+// (rsk / gsk), outputs plain.  Each lane computes 4 consecutive outputs over TP =
+// min(8, N) consecutive taps, sliding a 4-value window along the kernel: one kernel
+// load and one r load per 4 FMAs (the one-output-per-lane-group form was bound by its
+// 2 loads per FMA).  The P = N / TP tap parts of an output group sit in lanes Q = 32 / P
+// apart and are combined by an xor tree.  The order depends on N only.
+template <int TP>
+__device__ __forceinline__ void circulant_blocked_taps(const double *g, const double *r, int j0, int i0, int M,
+                                                       double &a0, double &a1, double &a2, double &a3) {
+    // every load issued up front (compile-time tap count): r[i0 .. i0+TP) and the TP + 3
+    // kernel values g[j0 + 3 - i0 - t'] the sliding window visits
+    double rv[TP], gv[TP + 3];
+#pragma unroll
+    for (int t = 0; t < TP; ++t) rv[t] = r[rsk(i0 + t)];
+#pragma unroll
+    for (int u = 0; u < TP + 3; ++u) gv[u] = g[gsk((j0 + 3 - i0 - u) & M)];
+    // tap t, output k: g[j0 + k - i0 - t] = gv[3 - k + t]
+#pragma unroll
+    for (int t = 0; t < TP; ++t) {
+        a0 = fma(gv[3 + t], rv[t], a0);
+        a1 = fma(gv[2 + t], rv[t], a1);
+        a2 = fma(gv[1 + t], rv[t], a2);
+        a3 = fma(gv[t], rv[t], a3);
+    }
+}
+
+static __device__ __forceinline__ void circulant_blocked(const double *gc, const double *gp, const double *r,
+                                                         double *c, double *phi, int N) {
+    // powers of two throughout: shifts and masks only (an integer division costs ~100s of cycles)
+    const int logN = 31 - __clz(N), logTP = logN < 3 ? logN : 3, logP = logN - logTP, logQ = 5 - logP;
+    const int TP = 1 << logTP, P = 1 << logP, Q = 1 << logQ, G = N >> 1;  // G groups of 4 outputs
+    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    const int part = ln >> logQ, gl = ln & (Q - 1), M = N - 1;
+    for (int wb = 0; wb * Q < G; wb += nw) {  // warp-uniform trip count
+        if ((wb + warp) * Q >= G) break;         // whole warp idle (warp-uniform)
+        const int grp = (wb + warp) * Q + gl;
+        const bool active = grp < G;
+        const int o0 = active ? 4 * grp : 0;
+        const bool isc = o0 < N;
+        const double *g = isc ? gc : gp;
+        const int j0 = isc ? o0 : o0 - N, i0 = part * TP;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        if (TP == 8)
+            circulant_blocked_taps<8>(g, r, j0, i0, M, a0, a1, a2, a3);
+        else  // N = 4
+            circulant_blocked_taps<4>(g, r, j0, i0, M, a0, a1, a2, a3);
+        for (int q = P >> 1; q > 0; q >>= 1) {
+            a0 += __shfl_xor_sync(0xffffffffu, a0, q * Q);
+            a1 += __shfl_xor_sync(0xffffffffu, a1, q * Q);
+            a2 += __shfl_xor_sync(0xffffffffu, a2, q * Q);
+            a3 += __shfl_xor_sync(0xffffffffu, a3, q * Q);
+        }
+        if (active && part == 0) {
+            double *dst = isc ? c : phi;
+            dst[j0] = a0;
+            dst[j0 + 1] = a1;
+            dst[j0 + 2] = a2;
+            dst[j0 + 3] = a3;
+        }
+    }
+}
+
 // c + i phi = IFFT_unscaled( FFT(r) * fac * (1 + i sym) ): the d = 1 Poisson solve +
 // spline fit in O(N log N) (fac = 1 / (N k^2 sym), 0 at the zero / Nyquist modes;
 // poisson.py:105-110, spline.py:78-84).  Both products are real-even factors on a
 // Hermitian spectrum, so c and phi come out as the real and imaginary parts of ONE
-// inverse transform.  tw: 2N shared doubles for the twiddles.
+// inverse transform.  twc / tws: the twiddles, already in shared memory; fq: this
+// thread's spectral factors (fac[k], fac[N+k], fac[kb], fac[N+kb]) for k = threadIdx.x,
+// loaded by the caller with its other global loads.
 static __device__ __forceinline__ void circulant_fft(const FieldParams &p, const double *r, double *c, double *phi,
-                                                     double *twc, double *tws, int N) {
+                                                     const double *twc, const double *tws, int N, const double fq[4]) {
     const int logN = 31 - __clz(N);
     for (int m = threadIdx.x; m < N; m += blockDim.x) {
-        twc[m] = p.twc[m];
-        tws[m] = p.tws[m];
         const int br = (int)(__brev((unsigned)m) >> (32 - logN));
         c[br] = r[m];
         phi[br] = 0.0;
@@ -324,7 +394,9 @@ static __device__ __forceinline__ void circulant_fft(const FieldParams &p, const
     for (int k = threadIdx.x; k < N; k += blockDim.x) {
         const int kb = (int)(__brev((unsigned)k) >> (32 - logN));
         if (k <= kb) {  // multiply and bit-reverse in place (disjoint swap pairs)
-            const double f0 = p.fac[k], s0 = p.fac[N + k], f1 = p.fac[kb], s1 = p.fac[N + kb];
+            const bool mine = k == (int)threadIdx.x;
+            const double f0 = mine ? fq[0] : p.fac[k], s0 = mine ? fq[1] : p.fac[N + k];
+            const double f1 = mine ? fq[2] : p.fac[kb], s1 = mine ? fq[3] : p.fac[N + kb];
             const double a0 = c[k] * f0, b0 = phi[k] * f0, a1 = c[kb] * f1, b1 = phi[kb] * f1;
             c[kb] = fma(-b0, s0, a0);
             phi[kb] = fma(a0, s0, b0);
@@ -341,31 +413,101 @@ static __device__ __forceinline__ void circulant_fft(const FieldParams &p, const
 // space), so the coefficient slab is one circular convolution c = gc (*) rho'
 // and the nodal potential phi = gp (*) rho' another; the electric energy follows
 // from Parseval, W = (L/N)/2 sum_i rho'_i phi_i = L/2 sum_alpha k^2 |phi_hat|^2
-// (poisson.py:115-120).  Two length-N convolutions replace two DFT pairs and
-// need far fewer barriers -- this routine sits on the latency-critical path of
-// every d = 1 step.
+// (poisson.py:115-120).  This routine sits on the latency-critical path of every
+// d = 1 step, so it is built around few dependent round trips:
+//   A  all threads: every global load issued before any is consumed (one L2 round
+//      trip), block sums of the tile-row partials, per-warp (min, max)      | barrier
+//   B  warp 0: rho, its mean, rho', the neutrality check, stats              | barrier
+//   C  all threads: the two convolutions (blocked direct N <= 64, else FFT)  | barrier
+//   D  last warp: W;  all threads: the appended slabs and E at the nodes.
 static __device__ __forceinline__ bool field_update_1d_body(const FieldParams &p, double *sm) {
     const int N = p.N, T = blockDim.x, B = p.B, rpb = p.rows_per_block;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = T >> 5;
+    const bool small = N <= 64;  // blocked direct convolution on skewed operands, else FFT
+    const int RS = small ? N + (N >> 3) : N, GS = small ? N + (N >> 2) : N;
+    // B N + RS + 2 GS + 2 N + 128 <= field_smem_doubles(N, N, true) = 14 N + 128 (B <= 8)
     double *sb = sm;            // B * N block sums
-    double *r = sb + B * N;     // rho (then neutral rho)
-    double *gc = r + N, *gp = gc + N, *c = gp + N, *phi = c + N;
-    double *scratch = phi + N;  // 64
+    double *r = sb + B * N;     // rho, then rho' (skewed when small)
+    double *gc = r + RS, *gp = gc + GS;  // kernels (skewed) or FFT twiddles
+    double *c = gp + GS, *phi = c + N;
+    double *scratch = phi + N;  // 128
     NUFI_STAMP(p, 0);
-    for (int m = threadIdx.x; m < N; m += T) {
-        gc[m] = p.gc[m];
-        gp[m] = p.gp[m];
+    // ---- A: with in-order issue a load feeding a store stalls the thread, so the kernel
+    // taps / twiddles, the spectral factors, the block (min, max) and the tile-row
+    // partials are all requested before anything is consumed ----
+    const int t0 = threadIdx.x;
+    const double *g0src = small ? p.gc : p.twc, *g1src = small ? p.gp : p.tws;
+    double ga = 0.0, gb = 0.0, fq[4] = {0.0, 0.0, 0.0, 0.0};
+    if (t0 < N) {
+        ga = __ldg(g0src + t0);
+        gb = __ldg(g1src + t0);
+        if (!small) {
+            const int kb = (int)(__brev((unsigned)t0) >> (32 - (31 - __clz(N))));
+            if (t0 <= kb) {
+                fq[0] = __ldg(p.fac + t0);
+                fq[1] = __ldg(p.fac + N + t0);
+                fq[2] = __ldg(p.fac + kb);
+                fq[3] = __ldg(p.fac + N + kb);
+            }
+        }
+    }
+    const int nmm = p.sums ? B * p.mm_per_block : 0;
+    double mn = DBL_MAX, mx = -DBL_MAX;
+    // Staged path: every tile-row partial and (min, max) pair is copied into shared memory
+    // with cp.async (16-byte chunks, no registers held, all in flight at once), then summed
+    // from there.  The register-load path below is limited by the compiler interleaving
+    // each load with its add (one L2 round trip per row).
+    const int64_t nsum = (int64_t)B * rpb * N;
+    const bool stage = p.sums && rpb > 1 && p.stage_cap >= nsum + 2 * (int64_t)nmm &&
+                       ((reinterpret_cast<uintptr_t>(p.sums) | reinterpret_cast<uintptr_t>(p.minmax)) & 15) == 0;
+    double *stg = sm + field_smem_doubles(N, N, true);  // even offset: 16-byte aligned
+    if (stage) {
+        for (int64_t q = t0; q < nsum / 2; q += T) cp_async16(stg + 2 * q, p.sums + 2 * q);
+        for (int q = t0; q < nmm; q += T) cp_async16(stg + nsum + 2 * q, p.minmax + 2 * q);
+        cp_async_wait_all();
+        __syncthreads();
+        // rows in order per output; rows in chunks of 8 with every load of a chunk issued
+        // before its adds (N a power of two: shifts only)
+        // two outputs per thread, their two add chains interleaved
+        const int logN = 31 - __clz(N), BN = B * N;
+        for (int it = t0; it < BN; it += 2 * T) {
+            const int it2 = it + T < BN ? it + T : it;
+            const double *s1 = stg + (size_t)(it >> logN) * rpb * N + (it & (N - 1));
+            const double *s2 = stg + (size_t)(it2 >> logN) * rpb * N + (it2 & (N - 1));
+            double S1 = 0.0, S2 = 0.0;
+            int q = 0;
+            for (; q + 8 <= rpb; q += 8) {
+                double a[8], b[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    a[u] = s1[(size_t)(q + u) * N];
+                    b[u] = s2[(size_t)(q + u) * N];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    S1 += a[u];
+                    S2 += b[u];
+                }
+            }
+            for (; q < rpb; ++q) {
+                S1 += s1[(size_t)q * N];
+                S2 += s2[(size_t)q * N];
+            }
+            sb[it] = S1;
+            if (it + T < BN) sb[it + T] = S2;
+        }
+        for (int q = t0; q < nmm; q += T) {
+            mn = fmin(mn, stg[nsum + 2 * q]);
+            mx = fmax(mx, stg[nsum + 2 * q + 1]);
+        }
+    } else if (t0 < nmm) {
+        mn = __ldcg(p.minmax + 2 * t0);
+        mx = __ldcg(p.minmax + 2 * t0 + 1);
     }
     // ---- block sums over the block's rows in order (reduce_blocks_kernel order) ----
-    double mn = DBL_MAX, mx = -DBL_MAX;
-    if (p.sums) {
-        for (int q = threadIdx.x; q < B * p.mm_per_block; q += T) {
-            mn = fmin(mn, __ldcg(p.minmax + 2 * q));
-            mx = fmax(mx, __ldcg(p.minmax + 2 * q + 1));
-        }
+    if (p.sums && !stage) {
         if (rpb <= 8) {
-            // two outputs per thread per pass: all 2 * rpb loads in flight at once (one L2
-            // round trip instead of two on the latency-critical path); same order as below
+            // two outputs per thread per pass: all 2 * rpb loads in flight at once
             for (int it = threadIdx.x; it < B * N; it += 2 * T) {
                 const int it2 = it + T;
                 const double *s1 = p.sums + (size_t)(it / N) * rpb * N + (it % N);
@@ -403,6 +545,12 @@ static __device__ __forceinline__ bool field_update_1d_body(const FieldParams &p
                 sb[it] = Sb;
             }
         }
+        for (int q = t0 + T; q < nmm; q += T) {
+            mn = fmin(mn, __ldcg(p.minmax + 2 * q));
+            mx = fmax(mx, __ldcg(p.minmax + 2 * q + 1));
+        }
+    }
+    if (p.sums) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
@@ -412,78 +560,97 @@ static __device__ __forceinline__ bool field_update_1d_body(const FieldParams &p
             scratch[warp] = mn;
             scratch[32 + warp] = mx;
         }
-    } else {
-        for (int i = threadIdx.x; i < N; i += T) r[i] = p.rho_in[i];
+    }
+    if (t0 < N) {
+        gc[small ? gsk(t0) : t0] = ga;
+        gp[small ? gsk(t0) : t0] = gb;
+    }
+    for (int m = t0 + T; m < N; m += T) {
+        gc[small ? gsk(m) : m] = __ldg(g0src + m);
+        gp[small ? gsk(m) : m] = __ldg(g1src + m);
     }
     __syncthreads();
     NUFI_STAMP(p, 1);
-    // ---- rho = rho_bar - hv S (density.py:81), mean and min / max in warp 0 ----
-    if (p.sums)
-        for (int i = threadIdx.x; i < N; i += T) {
-            double S = 0.0;
-            for (int b = 0; b < B; ++b) S += sb[b * N + i];
-            r[i] = p.rho_bar - p.hv_d * S;
-        }
-    __syncthreads();
-    // every warp forms the mean itself (identical order in every warp: no barrier and
-    // no shared-memory round trip), the neutral rho goes to the free block-sum array
-    double neut;
-    {
+    // ---- B (warp 0): rho = rho_bar - hv S (density.py:81), c = mean, rho' = rho - c
+    // (density.py:84-85), the neutrality check of poisson.py:97-104 on rho', stats ----
+    if (warp == 0) {
         double s = 0.0;
-        for (int i = lane; i < N; i += 32) s += r[i];
-        s = warp_sum(s);
-        neut = p.sums ? s / (double)N : 0.0;  // density.py:84
-    }
-    if (threadIdx.x == 0 && p.stats_out) {
-        double fmn = DBL_MAX, fmx = -DBL_MAX;
-        if (p.sums)
-            for (int w = 0; w < (T >> 5); ++w) {
-                fmn = fmin(fmn, scratch[w]);
-                fmx = fmax(fmx, scratch[32 + w]);
+        // two nodes per lane per pass (i, i + 32), their chains interleaved; s in node order
+        for (int i = lane; i < N; i += 64) {
+            const int i2 = i + 32 < N ? i + 32 : i;
+            double r1, r2;
+            if (p.sums) {
+                double S1 = 0.0, S2 = 0.0;
+                for (int b = 0; b < B; ++b) {
+                    S1 += sb[b * N + i];
+                    S2 += sb[b * N + i2];
+                }
+                r1 = p.rho_bar - p.hv_d * S1;
+                r2 = p.rho_bar - p.hv_d * S2;
+            } else {
+                r1 = p.rho_in[i];
+                r2 = p.rho_in[i2];
             }
-        p.stats_out[0] = neut;
-        p.stats_out[1] = fmn;
-        p.stats_out[2] = fmx;
+            r[small ? rsk(i) : i] = r1;
+            s += r1;
+            if (i + 32 < N) {
+                r[small ? rsk(i2) : i2] = r2;
+                s += r2;
+            }
+        }
+        s = warp_sum(s);
+        // N is a power of two here: s * (1/N) is s / N exactly (no DDIV on the critical path)
+        const double neut = p.sums ? s * (1.0 / (double)N) : 0.0;
+        double s2 = 0.0, m = 0.0;
+        for (int i = lane; i < N; i += 32) {
+            const int ix = small ? rsk(i) : i;
+            const double v = r[ix] - neut;
+            r[ix] = v;
+            if (p.rho_out) p.rho_out[i] = v;
+            s2 += v;
+            m = fmax(m, fabs(v));
+        }
+        s2 = warp_sum(s2);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (p.stats_out) {
+            double fmn = (p.sums && lane < nw) ? scratch[lane] : DBL_MAX;
+            double fmx = (p.sums && lane < nw) ? scratch[32 + lane] : -DBL_MAX;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                fmn = fmin(fmn, __shfl_xor_sync(0xffffffffu, fmn, o));
+                fmx = fmax(fmx, __shfl_xor_sync(0xffffffffu, fmx, o));
+            }
+            if (lane == 0) {
+                p.stats_out[0] = neut;
+                p.stats_out[1] = fmn;
+                p.stats_out[2] = fmx;
+            }
+        }
+        if (lane == 0) {
+            const bool bad = fabs(s2 * (1.0 / (double)N)) > 1e-8 * m;
+            scratch[96] = bad ? 1.0 : 0.0;
+            if (bad && p.status) *p.status = NUFI_ERR_NUMERICAL;
+        }
     }
-    double *rn = sb;  // B * N >= N doubles, no longer needed
-    for (int i = threadIdx.x; i < N; i += T) {
-        const double v = r[i] - neut;  // density.py:85
-        rn[i] = v;
-        if (p.rho_out) p.rho_out[i] = v;
-    }
-    r = rn;
     if (p.finish_only) return true;
     __syncthreads();
     NUFI_STAMP(p, 2);
-    // ---- c = gc (*) rho', phi = gp (*) rho': 2N outputs ----
-    if (N >= 128)
-        circulant_fft(p, r, c, phi, gc, gp, N);  // gc / gp smem reused for the twiddles
+    if (scratch[96] != 0.0) return false;  // history unchanged (the reference raises before appending)
+    // ---- C: c = gc (*) rho', phi = gp (*) rho' ----
+    if (small)
+        circulant_blocked(gc, gp, r, c, phi, N);
     else
-        circulant_direct(gc, gp, r, c, phi, N);
+        circulant_fft(p, r, c, phi, gc, gp, N, fq);
     __syncthreads();
     NUFI_STAMP(p, 4);
-    // ---- W (Parseval) and the neutrality check (poisson.py:97-104) in warp 0 ----
-    if (warp == 0) {
-        double w = 0.0, s = 0.0, m = 0.0;
-        for (int i = lane; i < N; i += 32) {
-            w = fma(r[i], phi[i], w);
-            s += r[i];
-            m = fmax(m, fabs(r[i]));
-        }
+    // ---- D: W (Parseval) in the last warp, which holds no append work for N < T ----
+    if (warp == nw - 1 && p.W_out) {
+        double w = 0.0;
+        for (int i = lane; i < N; i += 32) w = fma(r[small ? rsk(i) : i], phi[i], w);
         w = warp_sum(w);
-        s = warp_sum(s);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (lane == 0) {
-            const bool bad = fabs(s / (double)N) > 1e-8 * m;
-            scratch[1] = bad ? 1.0 : 0.0;
-            if (bad && p.status) *p.status = NUFI_ERR_NUMERICAL;
-            if (!bad && p.W_out) *p.W_out = 0.5 * (p.L / (double)N) * w;
-        }
+        if (lane == 0) *p.W_out = 0.5 * (p.L / (double)N) * w;
     }
-    __syncthreads();
-    NUFI_STAMP(p, 6);
-    if (scratch[1] != 0.0) return false;  // history unchanged (the reference raises before appending)
     // ---- append: raw slab, evaluation slab (trace_common.cuh layout), E at the nodes ----
     const double evs = p.slot == 0 ? 0.5 : 1.0;  // slab 0 stored pre-halved
     double *evg = p.ev_hist ? p.ev_hist + (size_t)p.slot * p.ev_slab_elems : nullptr;

@@ -120,6 +120,13 @@ __device__ __forceinline__ void fence_mbar_init() {
 
 // order this thread's (and, after a CTA barrier, the CTA's) generic-proxy shared-memory
 // accesses before subsequent async-proxy (TMA) accesses of the same bytes
+// cp.async (Ampere-style LDGSTS): a 16-byte global -> shared copy, L2 only (.cg), that
+// holds no registers while in flight; cp_async_wait_all waits for this thread's copies
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

@@ -400,6 +400,7 @@ __global__ void __launch_bounds__(288, 2) run_1d_kernel(const Run1DParams P) {
         // redundant tail in every CTA; CTA 0 publishes
         fp.slot = n;
         fp.ev_local = slabN;
+        fp.stage_cap = (int64_t)ring_doubles - field_smem_doubles(nodes, N, true);  // rest of the ring
         const int64_t row = n - P.n_first;
         if (lc == 0 && !(emu && rk != 0)) {  // one publisher per rank (emulated: rank 0 only)
             fp.rho_out = P.rho_hist ? P.rho_hist + row * nodes : nullptr;
