@@ -581,9 +581,23 @@ static __device__ __forceinline__ bool field_update_1d_body(const FieldParams &p
             double r1, r2;
             if (p.sums) {
                 double S1 = 0.0, S2 = 0.0;
-                for (int b = 0; b < B; ++b) {
-                    S1 += sb[b * N + i];
-                    S2 += sb[b * N + i2];
+                if (B == 8) {  // the usual block count: every load ahead of the ordered adds
+                    double a[8], c2[8];
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        a[b] = sb[b * N + i];
+                        c2[b] = sb[b * N + i2];
+                    }
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        S1 += a[b];
+                        S2 += c2[b];
+                    }
+                } else {
+                    for (int b = 0; b < B; ++b) {
+                        S1 += sb[b * N + i];
+                        S2 += sb[b * N + i2];
+                    }
                 }
                 r1 = p.rho_bar - p.hv_d * S1;
                 r2 = p.rho_bar - p.hv_d * S2;
@@ -613,24 +627,25 @@ static __device__ __forceinline__ bool field_update_1d_body(const FieldParams &p
         s2 = warp_sum(s2);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (p.stats_out) {
-            double fmn = (p.sums && lane < nw) ? scratch[lane] : DBL_MAX;
-            double fmx = (p.sums && lane < nw) ? scratch[32 + lane] : -DBL_MAX;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                fmn = fmin(fmn, __shfl_xor_sync(0xffffffffu, fmn, o));
-                fmx = fmax(fmx, __shfl_xor_sync(0xffffffffu, fmx, o));
-            }
-            if (lane == 0) {
-                p.stats_out[0] = neut;
-                p.stats_out[1] = fmn;
-                p.stats_out[2] = fmx;
-            }
-        }
+        if (p.stats_out && lane == 0) p.stats_out[0] = neut;
         if (lane == 0) {
             const bool bad = fabs(s2 * (1.0 / (double)N)) > 1e-8 * m;
             scratch[96] = bad ? 1.0 : 0.0;
             if (bad && p.status) *p.status = NUFI_ERR_NUMERICAL;
+        }
+    }
+    // sampled f min / max (the per-warp partials of phase A) in another warp, off warp 0's path
+    if (warp == (nw > 1 ? 1 : 0) && p.stats_out) {
+        double fmn = (p.sums && lane < nw) ? scratch[lane] : DBL_MAX;
+        double fmx = (p.sums && lane < nw) ? scratch[32 + lane] : -DBL_MAX;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            fmn = fmin(fmn, __shfl_xor_sync(0xffffffffu, fmn, o));
+            fmx = fmax(fmx, __shfl_xor_sync(0xffffffffu, fmx, o));
+        }
+        if (lane == 0) {
+            p.stats_out[1] = fmn;
+            p.stats_out[2] = fmx;
         }
     }
     if (p.finish_only) return true;
