@@ -62,3 +62,27 @@ def test_random_configuration_vs_oracle(seed):
     st = nufi.Simulation(grid, ic, tau, 5)
     outs = [st.step() for _ in range(6)]
     assert np.array_equal(np.stack([o.rho.reshape(-1) for o in outs]), res.rho[:6])
+
+
+@pytest.mark.parametrize("Nx", [4, 8, 16, 32, 64, 128, 256, 512])
+def test_d1_tail_every_power_of_two(Nx):
+    """The d = 1 step tail has size-specific paths (blocked direct convolution on skewed
+    operands for Nx <= 64, radix-2 FFT above, more nodes than threads from 512): each
+    against the oracle, and the persistent run == the single-step API bit for bit."""
+    L, tau, N = 4 * math.pi, 1 / 8, 12
+    prof_o = (O.Profile(centers=(0.0,), weights=(1.0,), power=0),)
+    case = O.Case(1, L, Nx, 16, 6.0, tau, 0.3, 0.5, prof_o)
+    ref = O.OracleRun(case).run(N)
+    grid = nufi.GridSpec(d=1, L=L, Nx=Nx, Nv=16, vmax=6.0)
+    ic = nufi.InitialCondition(benchmark=f"tail{Nx}", d=1, L=L, alpha=0.3, k=0.5,
+                               profiles=(nufi.VelocityProfile(),))
+    sim = nufi.Simulation(grid, ic, tau, N)
+    res = sim.run()
+    coeffs = sim.history.stacked().reshape(N + 1, -1)
+    assert normwise(res.rho, ref["rho"]).max() <= 1e-10
+    assert normwise(coeffs, ref["coeffs"]).max() <= 1e-10
+    assert np.all(np.abs(res.W - ref["W"]) <= 1e-8 * np.abs(ref["W"]) + 1e-300)
+    st = nufi.Simulation(grid, ic, tau, N)
+    outs = [st.step() for _ in range(N + 1)]
+    assert np.array_equal(np.stack([o.rho.reshape(-1) for o in outs]), res.rho)
+    assert np.array_equal(np.array([o.W for o in outs]), res.W)
