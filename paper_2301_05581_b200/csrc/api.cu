@@ -493,7 +493,9 @@ int nufi_create(const nufi_config *cfg, int device, void *stream, nufi_handle **
     }
     h->ev_elems = ev_slab_elems(c.d, c.Nx);
     h->f32 = (c.flags & NUFI_FLAG_F32_HISTORY) ? 1 : 0;
-    h->large = h->nodes > MAX_FIELD_NODES;
+    // beyond one CTA: too many nodes, or (d = 1, 14-16 work rows of N doubles) a single-CTA
+    // tail that would not fit the 227 KB of shared memory a CTA can have
+    h->large = h->nodes > MAX_FIELD_NODES || field_smem_doubles(h->nodes, c.Nx, c.d == 1) * sizeof(double) > 227 * 1024;
     choose_tiling(h);
     if (h->large && h->d == 1) h->gl = true;  // d = 1 beyond one CTA: generic in-place trace
 

@@ -104,7 +104,8 @@ struct Run1DParams {
 // shared-memory doubles the routine needs: 4 work arrays, twiddles, the
 // per-block sums (B <= 8 blocks staged when rows_per_block > 1), scratch
 __host__ __device__ constexpr int field_smem_doubles(int nodes, int N, bool staged) {
-    return 4 * nodes + 2 * N + (staged ? 8 * nodes : 0) + 128;  // scratch: 3 x 32 warp slots (cta_sum_min_max)
+    // staged (d = 1): + 8 block-sum rows and a 2N complex work buffer (circulant_fft4)
+    return 4 * nodes + 2 * N + (staged ? 8 * nodes + 2 * N : 0) + 128;  // scratch: 3 x 32 warp slots
 }
 
 // FP32 history mode: a stored coefficient is the float32 rounding of the fit
@@ -370,6 +371,146 @@ static __device__ __forceinline__ void circulant_blocked(const double *gc, const
             dst[j0 + 1] = a1;
             dst[j0 + 2] = a2;
             dst[j0 + 3] = a3;
+        }
+    }
+}
+
+// ---- four-step FFT for N = 16 R1 (R1 = 8, 16): two passes of in-register DFTs ----
+// cos / sin(2 pi j / 16), j < 8 (correctly rounded; the symmetric pairs exactly equal)
+#define NUFI_C1 0x1.d906bcf328d46p-1  // cos(pi/8)
+#define NUFI_S1 0x1.87de2a6aea963p-2  // sin(pi/8)
+#define NUFI_R2 0x1.6a09e667f3bcdp-1  // sqrt(2)/2
+__device__ __forceinline__ constexpr double tw16c(int j) {
+    return j == 0 ? 1.0 : j == 1 ? NUFI_C1 : j == 2 ? NUFI_R2 : j == 3 ? NUFI_S1 : j == 4 ? 0.0
+         : j == 5 ? -NUFI_S1 : j == 6 ? -NUFI_R2 : -NUFI_C1;
+}
+__device__ __forceinline__ constexpr double tw16s(int j) {
+    return j == 0 ? 0.0 : j == 1 ? NUFI_S1 : j == 2 ? NUFI_R2 : j == 3 ? NUFI_C1 : j == 4 ? 1.0
+         : j == 5 ? NUFI_C1 : j == 6 ? NUFI_R2 : NUFI_S1;
+}
+__device__ __forceinline__ constexpr int brev_c(int i, int bits) {
+    int r = 0;
+    for (int b = 0; b < bits; ++b) r |= ((i >> b) & 1) << (bits - 1 - b);
+    return r;
+}
+
+// In-register R-point DFT (R = 8, 16), X_k = sum_n x_n e^{SIGN 2 pi i n k / R}: radix-2
+// decimation in time on a bit-reversed copy, twiddles compile-time constants (the
+// trivial ones -- 1 and +-i -- are plain adds).
+template <int R, int SIGN>
+__device__ __forceinline__ void dft_reg(double (&re)[R], double (&im)[R]) {
+    constexpr int LOG = R == 16 ? 4 : 3;
+    double ar[R], ai[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        ar[i] = re[brev_c(i, LOG)];
+        ai[i] = im[brev_c(i, LOG)];
+    }
+#pragma unroll
+    for (int h = 1; h < R; h <<= 1) {
+#pragma unroll
+        for (int b = 0; b < R / 2; ++b) {
+            const int pos = b % h, i0 = (b / h) * 2 * h + pos, i1 = i0 + h;
+            const int t = pos * (16 / (2 * h));  // e^{SIGN 2 pi i pos / (2h)} = tw16[t]
+            double xr, xi;
+            if (t == 0) {
+                xr = ar[i1];
+                xi = ai[i1];
+            } else if (t == 4) {  // multiply by SIGN * i
+                xr = -SIGN * ai[i1];
+                xi = SIGN * ar[i1];
+            } else {
+                const double wr = tw16c(t), wi = SIGN * tw16s(t);
+                xr = fma(ar[i1], wr, -ai[i1] * wi);
+                xi = fma(ar[i1], wi, ai[i1] * wr);
+            }
+            ar[i1] = ar[i0] - xr;
+            ai[i1] = ai[i0] - xi;
+            ar[i0] = ar[i0] + xr;
+            ai[i0] = ai[i0] + xi;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        re[i] = ar[i];
+        im[i] = ai[i];
+    }
+}
+
+// One four-step transform, N = R1 * 16, n = n1 + R1 n2, k = k2 + 16 k1:
+//   pass 1 (thread n1 < R1): Y[n1][k2] = e^{SIGN 2 pi i n1 k2 / N} sum_n2 x[n1 + R1 n2] w16^{n2 k2}
+//   pass 2 (thread k2 < 16): X[k2 + 16 k1] = sum_n1 Y[n1][k2] w_R1^{n1 k1}
+// Y lives in (yr, yi) at k2 R1 + (n1 ^ (k2 & (R1 - 1))) (xor swizzle: both passes
+// conflict-free or 2-way); twc / tws: cos / sin(2 pi m / N) in shared memory.
+template <int R1, int SIGN>
+__device__ __forceinline__ void fft4_pass1(const double *xr, const double *xi, double *yr, double *yi,
+                                           const double *twc, const double *tws) {
+    const int n1 = threadIdx.x;
+    if (n1 >= R1) return;
+    double re[16], im[16];
+#pragma unroll
+    for (int n2 = 0; n2 < 16; ++n2) {
+        re[n2] = xr[n1 + R1 * n2];
+        im[n2] = xi ? xi[n1 + R1 * n2] : 0.0;
+    }
+    dft_reg<16, SIGN>(re, im);
+#pragma unroll
+    for (int k2 = 0; k2 < 16; ++k2) {
+        const int m = n1 * k2;  // < N
+        const double wr = twc[m], wi = SIGN * tws[m];
+        const int o = k2 * R1 + (n1 ^ (k2 & (R1 - 1)));
+        yr[o] = fma(re[k2], wr, -im[k2] * wi);
+        yi[o] = fma(re[k2], wi, im[k2] * wr);
+    }
+}
+
+template <int R1>
+__device__ __forceinline__ void fft4_pass2_load(const double *yr, const double *yi, double (&re)[R1],
+                                                double (&im)[R1]) {
+    const int k2 = threadIdx.x;
+#pragma unroll
+    for (int n1 = 0; n1 < R1; ++n1) {
+        const int o = k2 * R1 + (n1 ^ (k2 & (R1 - 1)));
+        re[n1] = yr[o];
+        im[n1] = yi[o];
+    }
+}
+
+// c + i phi = IFFT_unscaled( FFT(r) * fac * (1 + i sym) ) by two four-step transforms,
+// natural order throughout; wr / wi: 2N doubles of work space.  3 CTA barriers.
+template <int R1>
+static __device__ __forceinline__ void circulant_fft4(const FieldParams &p, const double *r, double *c, double *phi,
+                                                      const double *twc, const double *tws, double *wr,
+                                                      double *wi) {
+    constexpr int N = 16 * R1;
+    fft4_pass1<R1, -1>(r, nullptr, wr, wi, twc, tws);  // forward: r is real
+    __syncthreads();
+    if (threadIdx.x < 16) {
+        const int k2 = threadIdx.x;
+        double re[R1], im[R1];
+        fft4_pass2_load<R1>(wr, wi, re, im);
+        dft_reg<R1, -1>(re, im);
+#pragma unroll
+        for (int k1 = 0; k1 < R1; ++k1) {  // spectrum * fac * (1 + i sym) -> (c, phi), natural order
+            const int k = k2 + 16 * k1;
+            const double f = p.fac[k], sy = p.fac[N + k];
+            const double a = re[k1] * f, b = im[k1] * f;
+            c[k] = fma(-b, sy, a);
+            phi[k] = fma(a, sy, b);
+        }
+    }
+    __syncthreads();
+    fft4_pass1<R1, 1>(c, phi, wr, wi, twc, tws);  // inverse, unscaled
+    __syncthreads();
+    if (threadIdx.x < 16) {
+        const int k2 = threadIdx.x;
+        double re[R1], im[R1];
+        fft4_pass2_load<R1>(wr, wi, re, im);
+        dft_reg<R1, 1>(re, im);
+#pragma unroll
+        for (int k1 = 0; k1 < R1; ++k1) {
+            c[k2 + 16 * k1] = re[k1];
+            phi[k2 + 16 * k1] = im[k1];
         }
     }
 }
@@ -655,6 +796,10 @@ static __device__ __forceinline__ bool field_update_1d_body(const FieldParams &p
     // ---- C: c = gc (*) rho', phi = gp (*) rho' ----
     if (small)
         circulant_blocked(gc, gp, r, c, phi, N);
+    else if (N == 256)
+        circulant_fft4<16>(p, r, c, phi, gc, gp, scratch + 128, scratch + 128 + N);
+    else if (N == 128)
+        circulant_fft4<8>(p, r, c, phi, gc, gp, scratch + 128, scratch + 128 + N);
     else
         circulant_fft(p, r, c, phi, gc, gp, N, fq);
     __syncthreads();

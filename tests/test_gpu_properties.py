@@ -64,10 +64,11 @@ def test_random_configuration_vs_oracle(seed):
     assert np.array_equal(np.stack([o.rho.reshape(-1) for o in outs]), res.rho[:6])
 
 
-@pytest.mark.parametrize("Nx", [4, 8, 16, 32, 64, 128, 256, 512])
+@pytest.mark.parametrize("Nx", [4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096])
 def test_d1_tail_every_power_of_two(Nx):
     """The d = 1 step tail has size-specific paths (blocked direct convolution on skewed
-    operands for Nx <= 64, radix-2 FFT above, more nodes than threads from 512): each
+    operands for Nx <= 64, four-step FFT for 128 and 256, radix-2 FFT above, more nodes than
+    threads from 512, the multi-CTA tail once one CTA cannot hold the work rows): each
     against the oracle, and the persistent run == the single-step API bit for bit."""
     L, tau, N = 4 * math.pi, 1 / 8, 12
     prof_o = (O.Profile(centers=(0.0,), weights=(1.0,), power=0),)
