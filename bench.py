@@ -179,8 +179,11 @@ def smem_roofline(torch, dev, d, trace_ps, trace_ms):
     return {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak if achieved else None,
             "peak_source": f"nominal: 128 B/clk/SM x {sms} SMs x {mhz:.0f} MHz",
-            "note": "d=1 reads 24 B/point-step (A,B,C cell polynomial) against the 32 B algorithmic figure; "
-                    "random late-time gathers cost ~3.75 wavefronts per 8-byte warp load (ncu, profiles/)"}
+            "note": ("d=1 reads 24 B/point-step (A,B,C cell polynomial) against the 32 B algorithmic figure; "
+                     "random late-time gathers cost ~3.75 wavefronts per 8-byte warp load (ncu, profiles/)")
+            if d == 1 else
+            (f"d={d} reads exactly the {ALGO_BYTES[d]} B of the 4^d stencil per point-step, conflict-free "
+             "(2.0 wavefronts per 8-byte warp load, ncu, profiles/); co-bound with the FP64 pipe")}
 
 
 def flush_l2(torch, buf):
