@@ -256,34 +256,6 @@ __device__ __forceinline__ void fft_axis_pass(const double *__restrict__ ire, co
     }
 }
 
-// c = gc (*) r and phi = gp (*) r for small N (power of two): one output per
-// group of G lanes, conflict-free kernel-tap loads (consecutive j across groups).
-static __device__ __forceinline__ void circulant_direct(const double *gc, const double *gp, const double *r, double *c,
-                                                        double *phi, int N) {
-    const int T = blockDim.x;
-    // lanes per output from N alone (the values the old T = 256 / 288 rule gave), so
-    // the summation order -- and the bits -- never depend on the CTA size
-    int G = 128 / N < N / 2 ? 128 / N : N / 2;
-    G = G < 1 ? 1 : (G > 32 ? 32 : G);
-    const int part = threadIdx.x % G;
-    for (int base = 0; base < 2 * N; base += T / G) {  // warp-uniform trip count
-        const int o = base + threadIdx.x / G;
-        const bool active = o < 2 * N;
-        const int j = !active ? 0 : (o < N ? o : o - N);
-        const double *g = o < N ? gc : gp;
-        double a0 = 0.0, a1 = 0.0;
-        int i = part;
-        for (; i + G < N; i += 2 * G) {
-            a0 = fma(g[(j - i + N) & (N - 1)], r[i], a0);
-            a1 = fma(g[(j - i - G + N) & (N - 1)], r[i + G], a1);
-        }
-        if (i < N) a0 = fma(g[(j - i + N) & (N - 1)], r[i], a0);
-        double a = a0 + a1;
-        for (int q = G >> 1; q > 0; q >>= 1) a += __shfl_xor_sync(0xffffffffu, a, q, G);
-        if (active && part == 0) (o < N ? c : phi)[j] = a;
-    }
-}
-
 // In-place radix-2 complex FFT of length N = 2^logN on shared arrays (re, im) whose
 // input is already in bit-reversed order; sign -1: forward e^{-2 pi i jk/N}, +1:
 // unscaled inverse.  twc / tws: cos / sin(2 pi m / N), m < N.  One butterfly per
