@@ -202,6 +202,17 @@ int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, d
 int nufi_trace(nufi_handle *h, int64_t n, double *X, double *V, int64_t M, int half_kick, int mode,
                int64_t *evals);
 
+/* FlowContext.install_field(step, UniformField(E0)) (flow.py:44-47, spline.py:55-68):
+ * a spatially constant field E0 (d values) overrides stored field `step` for the
+ * point-level trace; E0 == NULL removes the override, nufi_clear_fields removes all.
+ * While any override is installed, nufi_trace follows the reference's generic path
+ * (flow.py:65-82: numpy operation order, UniformField or the stored spline's
+ * eval_E_many per slot; a slot needs a stored or installed field), and the density /
+ * run entry points (nufi_rho*, nufi_step*, nufi_run, nufi_moments) return
+ * NUFI_ERR_USAGE. */
+int nufi_set_uniform_field(nufi_handle *h, int64_t step, const double *E0);
+int nufi_clear_fields(nufi_handle *h);
+
 /* Observable sweep at step n (density.quadrature_sweep_many, density.py:94-120,
  * for the conserved-quantity weights of SPEC.md:403-406): every quadrature
  * point of this handle's velocity blocks is traced with Psi (needs len >= n+1

@@ -328,6 +328,36 @@ def trace_numpy(coeffs, L, n, tau, X, V, half_kick) -> int:
     return evals
 
 
+def trace_generic(fields, L, n, tau, X, V, half_kick) -> int:
+    """flow.py:65-82 (_trace_generic), the reference's trace whenever a non-spline field is
+    installed (flow.py:44-47): fields[k] is a stored coefficient slab (SplineField,
+    eval_E_many = kernels.py:102-123) or ("uniform", E0) (UniformField, spline.py:55-68)."""
+    if n == 0:
+        return 0
+    M = X.shape[0]
+
+    def E(k):
+        f = fields[k]
+        if isinstance(f, tuple) and f[0] == "uniform":
+            return np.broadcast_to(np.asarray(f[1], dtype=np.float64), (M, X.shape[1])).copy()
+        return eval_E_many(f, L, X)
+
+    evals = 0
+    if half_kick:
+        V += (0.5 * tau) * E(n)
+        evals += M
+    k = n
+    while k > 1:
+        k -= 1
+        X -= tau * V
+        V += tau * E(k)
+        evals += M
+    X -= tau * V
+    V += (0.5 * tau) * E(0)
+    evals += M
+    return evals
+
+
 # ---------------------------------------------------------------------------
 # poisson.py / spline.py
 # ---------------------------------------------------------------------------

@@ -17,6 +17,6 @@ from .flow import (TRACE_FAST, TRACE_PARITY, FlowContext, eval_f, eval_f0, eval_
 from .grids import GridSpec, PhasePoint, v_mid, v_mid_matrix, x_node, x_node_matrix
 from .initial import BENCHMARK_DEFAULTS, InitialCondition, VelocityProfile, make_benchmark, weak_landau_3d
 from .poisson import SpectralField, electric_energy, solve_poisson, wavenumber_squared
-from .spline import PotentialHistory, SplineField, fit_spline
+from .spline import PotentialHistory, SplineField, UniformField, fit_spline
 
 __version__ = "0.1.0"

@@ -102,6 +102,8 @@ _SIGS = {
     "nufi_trace": [_P, _I64, _P, _P, _I64, ctypes.c_int, ctypes.c_int, _I64P],
     "nufi_eval_f0": [_P, _P, _P, _I64, _P],
     "nufi_eval_field": [_P, _I64, _P, _I64, _P, _P],
+    "nufi_set_uniform_field": [_P, _I64, _P],
+    "nufi_clear_fields": [_P],
     "nufi_solve_poisson": [_P, _P, _P, _P, _P, _P],
     "nufi_fit_spline": [_P, _P, _P],
     "nufi_moments": [_P, _I64, _P, _I64P],

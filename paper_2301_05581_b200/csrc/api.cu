@@ -13,6 +13,7 @@
 #include <mutex>
 #include <utility>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "field_common.cuh"
@@ -26,6 +27,9 @@ cudaError_t launch_sweep_moments(int d, int ppt, bool pow2, const TraceRhoParams
 cudaError_t launch_reduce_moments(const double *part, int rows, int d, double measure, double *out, cudaStream_t st);
 cudaError_t launch_reduce_blocks(const double *partial, const double *fminmax, double *out, int nodes,
                                  int node_tiles, int vt_per_block, int b_lo, int b_hi, int B, cudaStream_t st);
+cudaError_t launch_trace_points_generic(int d, const double *hist, int nodes, const double *ovr, int N, double L,
+                                        int n, double tau, double *X, double *V, int64_t M, int half_kick,
+                                        cudaStream_t st);
 cudaError_t launch_trace_points(int d, int mode, bool pow2, const double *hist, const double *ev_hist,
                                 int ev_slab_elems, int N, int nodes, double L, int n, double tau, double K, double *X,
                                 double *V, int64_t M, int half_kick, cudaStream_t st);
@@ -126,6 +130,10 @@ struct nufi_handle {
     double *mg_part[NUFI_MG_MAX] = {}, *mg_fmm[NUFI_MG_MAX] = {};  // emulated ranks' partials
     unsigned *mg_bar[NUFI_MG_MAX] = {};
     int *mg_error = nullptr;
+    // installed non-spline fields (FlowContext.install_field, flow.py:44-47): per step
+    // [flag, E0_x, E0_y, E0_z]; honoured by the point-level trace (the reference's generic path)
+    std::vector<double> ovr;
+    int64_t n_ovr = 0;
 
     int64_t len = 0;  // host mirror of the history length
     bool large = false;   // Nx^d > MAX_FIELD_NODES: multi-CTA tail (field_large.cu)
@@ -831,8 +839,40 @@ static int copy_step_outputs(nufi_handle *h, double *rho_out, double *E_out, dou
 
 extern "C" {
 
+// installed fields are a test hook of the point-level flow (flow.py:44-82); the fused
+// density / run kernels trace stored splines only
+static int refuse_installed(nufi_handle *h) {
+    if (h->n_ovr > 0)
+        return fail(NUFI_ERR_USAGE, "installed (non-spline) fields are honoured by the point-level trace only; "
+                                    "clear them before compute_rho / run / step");
+    return NUFI_OK;
+}
+
+int nufi_set_uniform_field(nufi_handle *h, int64_t step, const double *E0) {
+    CHECK_HANDLE(h);
+    if (step < 0) return fail(NUFI_ERR_USAGE, "step index must be >= 0");
+    if ((size_t)(4 * (step + 1)) > h->ovr.size()) h->ovr.resize(4 * (size_t)(step + 1), 0.0);
+    const bool was = h->ovr[4 * step] != 0.0;
+    if (E0) {
+        h->ovr[4 * step] = 1.0;
+        for (int a = 0; a < 3; ++a) h->ovr[4 * step + 1 + a] = a < h->d ? E0[a] : 0.0;
+    } else {
+        for (int a = 0; a < 4; ++a) h->ovr[4 * step + a] = 0.0;
+    }
+    h->n_ovr += (E0 ? 1 : 0) - (was ? 1 : 0);
+    return NUFI_OK;
+}
+
+int nufi_clear_fields(nufi_handle *h) {
+    CHECK_HANDLE(h);
+    h->ovr.clear();
+    h->n_ovr = 0;
+    return NUFI_OK;
+}
+
 int nufi_rho_partials(nufi_handle *h, int64_t n, double *partials, int64_t *evals) {
     CHECK_HANDLE(h);
+    if (int rc = refuse_installed(h)) return rc;
     if (n < 0) return fail(NUFI_ERR_USAGE, "step index must be >= 0");
     if (n > 0 && h->len < n) return usage_history(h, n);
     if (!is_device_ptr(partials)) return fail(NUFI_ERR_USAGE, "partials must be a device buffer");
@@ -864,6 +904,7 @@ int nufi_rho_finish(nufi_handle *h, const double *partials, double *rho_out, dou
 
 int nufi_rho(nufi_handle *h, int64_t n, double *rho_out, double *stats3, int64_t *evals) {
     CHECK_HANDLE(h);
+    if (int rc = refuse_installed(h)) return rc;
     if (n < 0) return fail(NUFI_ERR_USAGE, "step index must be >= 0");
     if (n > 0 && h->len < n) return usage_history(h, n);
     StepOut o;
@@ -900,6 +941,7 @@ int nufi_field_update(nufi_handle *h, const double *rho, double *W_out, double *
 int nufi_step(nufi_handle *h, int64_t n, double *rho_out, double *E_out, double *W_out, double *stats3,
               int64_t *evals) {
     CHECK_HANDLE(h);
+    if (int rc = refuse_installed(h)) return rc;
     if (n != h->len) {
         char buf[160];
         snprintf(buf, sizeof buf, "step %lld requires a history of exactly %lld fields, have %lld", (long long)n,
@@ -1065,6 +1107,7 @@ int nufi_mg_handle_size(void) { return (int)sizeof(cudaIpcMemHandle_t); }
 int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, double *W_hist, double *stats_hist,
              int64_t *evals) {
     CHECK_HANDLE(h);
+    if (int rc = refuse_installed(h)) return rc;
     const int64_t first = h->len;
     if (n_last < first) return NUFI_OK;
     if (n_last >= h->cap) return fail(NUFI_ERR_USAGE, "n_last exceeds n_max");
@@ -1256,7 +1299,23 @@ int nufi_trace(nufi_handle *h, int64_t n, double *X, double *V, int64_t M, int h
     if (mode != NUFI_TRACE_FAST && mode != NUFI_TRACE_PARITY) return fail(NUFI_ERR_USAGE, "unknown trace mode");
     if (n == 0) return NUFI_OK;  // kernels.py:397-398
     const int64_t need = half_kick ? n + 1 : n;
-    if (h->len < need) {
+    if (h->n_ovr > 0) {
+        // flow.py:55-62 with installed fields: have = max(len, 1 + max installed step); a
+        // slot that is neither stored nor installed cannot be evaluated (history.entry)
+        int64_t top = -1;
+        for (int64_t k = 0; 4 * k < (int64_t)h->ovr.size(); ++k)
+            if (h->ovr[4 * k] != 0.0) top = k;
+        const int64_t have = std::max<int64_t>(h->len, top + 1);
+        bool missing = have < need;
+        for (int64_t k = h->len; k < need && !missing; ++k)
+            missing = 4 * k >= (int64_t)h->ovr.size() || h->ovr[4 * k] == 0.0;
+        if (missing) {
+            char buf[160];
+            snprintf(buf, sizeof buf, "trace at step %lld needs fields 0..%lld; history holds %lld", (long long)n,
+                     (long long)(need - 1), (long long)have);
+            return fail(NUFI_ERR_USAGE, buf);
+        }
+    } else if (h->len < need) {
         char buf[160];
         snprintf(buf, sizeof buf, "need %lld stored fields for step %lld, have %lld", (long long)need, (long long)n,
                  (long long)h->len);  // kernels.py:399-402
@@ -1271,8 +1330,20 @@ int nufi_trace(nufi_handle *h, int64_t n, double *X, double *V, int64_t M, int h
     if (!dv) CU(cudaMallocAsync(&dV, bytes, h->stream));
     if (!dx) CU(cudaMemcpyAsync(dX, X, bytes, cudaMemcpyHostToDevice, h->stream));
     if (!dv) CU(cudaMemcpyAsync(dV, V, bytes, cudaMemcpyHostToDevice, h->stream));
-    CU(launch_trace_points(h->d, mode, h->pow2, h->hist, h->ev_hist, h->ev_elems, h->N, h->nodes, h->cfg.L, (int)n,
-                           h->cfg.tau, h->K, dX, dV, M, half_kick ? 1 : 0, h->stream));
+    double *dovr = nullptr;
+    if (h->n_ovr > 0) {
+        // the reference's generic path (flow.py:65-82): every slot through its field object
+        std::vector<double> tab(4 * (size_t)(n + 1), 0.0);
+        std::copy(h->ovr.begin(), h->ovr.begin() + std::min(h->ovr.size(), tab.size()), tab.begin());
+        CU(cudaMallocAsync(&dovr, tab.size() * sizeof(double), h->stream));
+        CU(cudaMemcpyAsync(dovr, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        CU(launch_trace_points_generic(h->d, h->hist, h->nodes, dovr, h->N, h->cfg.L, (int)n, h->cfg.tau, dX, dV, M,
+                                       half_kick ? 1 : 0, h->stream));
+        CU(cudaFreeAsync(dovr, h->stream));
+    } else {
+        CU(launch_trace_points(h->d, mode, h->pow2, h->hist, h->ev_hist, h->ev_elems, h->N, h->nodes, h->cfg.L,
+                               (int)n, h->cfg.tau, h->K, dX, dV, M, half_kick ? 1 : 0, h->stream));
+    }
     if (!dx) CU(cudaMemcpyAsync(X, dX, bytes, cudaMemcpyDeviceToHost, h->stream));
     if (!dv) CU(cudaMemcpyAsync(V, dV, bytes, cudaMemcpyDeviceToHost, h->stream));
     if (!dx) CU(cudaFreeAsync(dX, h->stream));
@@ -1284,6 +1355,7 @@ int nufi_trace(nufi_handle *h, int64_t n, double *X, double *V, int64_t M, int h
 
 int nufi_moments(nufi_handle *h, int64_t n, double *out, int64_t *evals) {
     CHECK_HANDLE(h);
+    if (int rc = refuse_installed(h)) return rc;
     if (n < 0) return fail(NUFI_ERR_USAGE, "step index must be >= 0");
     if (!out) return fail(NUFI_ERR_USAGE, "null output");
     if (n > 0 && h->len < n + 1) {

@@ -196,17 +196,14 @@ __global__ void trace_points_fast(const double *__restrict__ ev_hist, int ev_sla
 // itertools.product order (x tap slowest), phi += c * prod w, E_g -= c * prod (dw on axis
 // g, w elsewhere), E *= N / L; elementwise IEEE operations in numpy's order, no FMA.
 template <int D>
-__global__ void eval_field_kernel(const double *__restrict__ c, int N, double L, const double *__restrict__ X,
-                                  int64_t M, double *__restrict__ phi_out, double *__restrict__ E_out) {
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= M) return;
-    const double inv_h = (double)N / L;
+__device__ __forceinline__ void field_numpy(const double *__restrict__ c, int N, double L, double inv_h,
+                                            const double *x, double *phi_out, double *E_out) {
     int i[D];
     double w[D][4], dw[D][4];
 #pragma unroll
     for (int a = 0; a < D; ++a) {
         double f;
-        cell_1d_exact(X[p * D + a], L, N, inv_h, i[a], f);
+        cell_1d_exact(x[a], L, N, inv_h, i[a], f);
         fill_weights_exact(f, w[a], dw[a]);
     }
     double phi = 0.0, E[D];
@@ -240,10 +237,71 @@ __global__ void eval_field_kernel(const double *__restrict__ c, int N, double L,
             E[g] = S_(E[g], v);
         }
     }
-    if (phi_out) phi_out[p] = phi;
+    if (phi_out) *phi_out = phi;
     if (E_out)
 #pragma unroll
-        for (int g = 0; g < D; ++g) E_out[p * D + g] = M_(E[g], inv_h);
+        for (int g = 0; g < D; ++g) E_out[g] = M_(E[g], inv_h);
+}
+
+template <int D>
+__global__ void eval_field_kernel(const double *__restrict__ c, int N, double L, const double *__restrict__ X,
+                                  int64_t M, double *__restrict__ phi_out, double *__restrict__ E_out) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= M) return;
+    double x[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) x[a] = X[p * D + a];
+    field_numpy<D>(c, N, L, (double)N / L, x, phi_out ? phi_out + p : nullptr, E_out ? E_out + p * D : nullptr);
+}
+
+// The reference's generic trace (flow.py:65-82), used there whenever a non-spline field is
+// installed (FlowContext.install_field, flow.py:44-47): numpy operation order --
+// V += (0.5 tau) E_n(X) [half kick]; k = n-1 .. 1: X -= tau V, V += tau E_k(X); X -= tau V,
+// V += (0.5 tau) E_0(X) -- where E_k is the installed UniformField (spline.py:55-68,
+// ovr[4k] != 0, E0 = ovr[4k+1 ..]) or the stored spline's eval_E_many.
+template <int D>
+__global__ void trace_points_generic(const double *__restrict__ hist, int nodes, const double *__restrict__ ovr,
+                                     int N, double L, int n, double tau, double *X, double *V, int64_t M,
+                                     int half_kick) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= M) return;
+    const double inv_h = (double)N / L;
+    const double half = M_(0.5, tau);
+    double x[D], v[D], E[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        x[a] = X[p * D + a];
+        v[a] = V[p * D + a];
+    }
+    auto field = [&](int k) {
+        if (ovr[4 * (size_t)k] != 0.0) {
+#pragma unroll
+            for (int a = 0; a < D; ++a) E[a] = ovr[4 * (size_t)k + 1 + a];
+        } else {
+            field_numpy<D>(hist + (size_t)k * nodes, N, L, inv_h, x, nullptr, E);
+        }
+    };
+    if (half_kick) {
+        field(n);
+#pragma unroll
+        for (int a = 0; a < D; ++a) v[a] = A_(v[a], M_(half, E[a]));
+    }
+    for (int k = n - 1; k >= 1; --k) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) x[a] = S_(x[a], M_(tau, v[a]));
+        field(k);
+#pragma unroll
+        for (int a = 0; a < D; ++a) v[a] = A_(v[a], M_(tau, E[a]));
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a) x[a] = S_(x[a], M_(tau, v[a]));
+    field(0);
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        v[a] = A_(v[a], M_(half, E[a]));
+        X[p * D + a] = x[a];
+        V[p * D + a] = v[a];
+    }
 }
 
 #undef M_
@@ -298,6 +356,17 @@ cudaError_t launch_trace_points(int d, int mode, bool pow2, const double *hist, 
         NUFI_TP(3)
 #undef NUFI_TP
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_trace_points_generic(int d, const double *hist, int nodes, const double *ovr, int N, double L,
+                                        int n, double tau, double *X, double *V, int64_t M, int half_kick,
+                                        cudaStream_t st) {
+    const int threads = 128;
+    const int ctas = (int)((M + threads - 1) / threads);
+    if (d == 1) trace_points_generic<1><<<ctas, threads, 0, st>>>(hist, nodes, ovr, N, L, n, tau, X, V, M, half_kick);
+    if (d == 2) trace_points_generic<2><<<ctas, threads, 0, st>>>(hist, nodes, ovr, N, L, n, tau, X, V, M, half_kick);
+    if (d == 3) trace_points_generic<3><<<ctas, threads, 0, st>>>(hist, nodes, ovr, N, L, n, tau, X, V, M, half_kick);
     return cudaGetLastError();
 }
 

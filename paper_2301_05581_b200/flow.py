@@ -6,9 +6,10 @@ eval_f_batch, point versions, and the field_evals counter.  The trace itself
 runs in libnufi_b200 (nufi_trace -> csrc/trace_points.cu); f0 is evaluated on
 the device (nufi_eval_f0).
 
-`install_field` (flow.py:44-47, a Python-level test hook that routes the trace
-through arbitrary field objects) is not offered on the GPU path; constant-force
-closed forms are tested through histories whose slabs produce that field.
+`install_field` (flow.py:44-47, the reference's test hook that overrides a stored
+field) takes UniformField objects (spline.py:55-68): while any is installed, the
+point-level trace follows the reference's generic path (flow.py:65-82) on the GPU
+(csrc/trace_points.cu trace_points_generic), for the constant-force closed-form tests.
 """
 
 from __future__ import annotations
@@ -52,6 +53,29 @@ class FlowContext:
 
     def reset_counter(self) -> None:
         self.field_evals = 0
+
+    def install_field(self, step: int, fld) -> None:
+        """Override the stored field at one step (flow.py:44-47, testing hook).  Accepts a
+        UniformField (or None to remove the override); the override lives on the history
+        (its device handle), so every context over that history sees it."""
+        from .spline import UniformField
+
+        if int(step) < 0:
+            raise UsageError("step index must be >= 0")
+        if fld is None:
+            self.history.handle.call("nufi_set_uniform_field", int(step), None)
+            return
+        if not isinstance(fld, UniformField):
+            raise UsageError("the GPU trace accepts UniformField overrides only (spline fields are stored "
+                             "with PotentialHistory.append)")
+        if fld.d != self.grid.d:
+            raise UsageError(f"UniformField has {fld.d} components, the grid has d = {self.grid.d}")
+        E0 = np.ascontiguousarray(fld.E0, dtype=np.float64)
+        self.history.handle.call("nufi_set_uniform_field", int(step), E0.ctypes.data)
+
+    def clear_fields(self) -> None:
+        """Remove every installed override."""
+        self.history.handle.call("nufi_clear_fields")
 
 
 def _batch(x, v, d: int):

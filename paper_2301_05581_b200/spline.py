@@ -69,6 +69,20 @@ class SplineField:
         return self._eval(X, False)
 
 
+class UniformField:
+    """A spatially constant electric field (spline.py:55-68).  No periodic potential
+    generates it; it exists for flow tests against the constant-force closed form and is
+    installed with FlowContext.install_field.  Only E evaluation is defined."""
+
+    def __init__(self, E0):
+        self.E0 = np.atleast_1d(np.asarray(E0, dtype=np.float64))
+        self.d = self.E0.shape[0]
+
+    def eval_E_many(self, X) -> np.ndarray:
+        X = np.atleast_2d(np.asarray(X, dtype=np.float64))
+        return np.broadcast_to(self.E0, (X.shape[0], self.d)).copy()
+
+
 def fit_spline(phi_nodes, grid: GridSpec, dtype=np.float64) -> SplineField:
     """Interpolating periodic cubic spline through nodal values (spline.py:71-86), on the GPU."""
     if grid.Nx < 4:

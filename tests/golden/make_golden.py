@@ -269,6 +269,44 @@ def field_goldens():
                             phi=fld.eval_phi_many(X), E=fld.eval_E_many(X))
 
 
+HOOK_CASES = {"kat_wl": (12, (3, 7)), "tiny2": (8, (2, 5)), "tiny3": (6, (1, 4))}
+
+
+def hook_goldens():
+    """FlowContext.install_field(step, UniformField(E0)) (flow.py:44-47, spline.py:55-68):
+    the reference's generic trace (flow.py:65-82) through a stored history with two slots
+    overridden, psi_batch and psi_tilde_batch at seeded points; plus the all-uniform
+    constant-force case (SPEC.md:309)."""
+    from vpflow import flow, spline
+
+    for base, (n, slots) in HOOK_CASES.items():
+        g, ic = build(CONFIGS[base])
+        tau = CONFIGS[base]["tau"]
+        z = np.load(os.path.join(OUT, f"{base}.npz"))
+        stack = z["coeffs"].reshape((-1,) + (g.Nx,) * g.d)[: n + 1]
+        hist = spline.PotentialHistory(g, tau)
+        for c in stack:
+            hist.append(spline.SplineField(grid=g, coeffs=np.ascontiguousarray(c)))
+        ctx = flow.FlowContext(history=hist, ic=ic, tau=tau, grid=g)
+        rng = np.random.default_rng(2024)
+        E0 = rng.uniform(-0.4, 0.4, (len(slots), g.d))
+        for s_, e in zip(slots, E0):
+            ctx.install_field(s_, spline.UniformField(e))
+        x = rng.uniform(-g.L, 2 * g.L, (400, g.d))
+        v = rng.uniform(-g.vmax, g.vmax, (400, g.d))
+        X1, V1 = flow.psi_batch(ctx, n, x, v)
+        X0, V0 = flow.psi_tilde_batch(ctx, n, x, v)
+        # all slots uniform: the constant-force closed form
+        ctx_u = flow.FlowContext(history=spline.PotentialHistory(g, tau), ic=ic, tau=tau, grid=g)
+        Eu = rng.uniform(-0.4, 0.4, g.d)
+        for k in range(n + 1):
+            ctx_u.install_field(k, spline.UniformField(Eu))
+        XU, VU = flow.psi_batch(ctx_u, n, x, v)
+        np.savez_compressed(os.path.join(OUT, f"hook_{base}.npz"), n=np.array(n), slots=np.array(slots), E0=E0,
+                            x=x, v=v, X_psi=X1, V_psi=V1, X_tilde=X0, V_tilde=V0, E_uniform=Eu, X_uniform=XU,
+                            V_uniform=VU, evals=np.array(ctx.field_evals))
+
+
 def host_info():
     try:
         cpu = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
@@ -289,6 +327,9 @@ def main(argv):
             continue
         if name == "checkpoints":
             checkpoint_goldens()
+            continue
+        if name == "hooks":
+            hook_goldens()
             continue
         if name.startswith("sweep_"):
             base = name[len("sweep_"):]

@@ -136,3 +136,24 @@ def test_sweep_vs_reference(name):
         scale = np.abs(ref[:4]).max()
         assert np.abs(got - ref).max() <= 1e-12 * scale, (n, got - ref)
         assert run.field_evals == int(z["field_evals"][i])
+
+
+@pytest.mark.parametrize("base", ["kat_wl", "tiny2", "tiny3"])
+def test_generic_trace_matches_reference_install_field(base):
+    """flow.py:65-82 with UniformField overrides (flow.py:44-47): the oracle's restatement
+    against the reference's own output (tests/golden/hook_*.npz), bit for bit."""
+    z = golden(f"hook_{base}")
+    ref = golden(base)
+    c = O.case(base)
+    n = int(z["n"])
+    stack = ref["coeffs"].reshape((-1,) + (c.Nx,) * c.d)
+    fields = {k: stack[k] for k in range(n + 1)}
+    for s, e in zip(z["slots"], z["E0"]):
+        fields[int(s)] = ("uniform", e)
+    for half, kx, kv in ((True, "X_psi", "V_psi"), (False, "X_tilde", "V_tilde")):
+        X, V = z["x"].copy(), z["v"].copy()
+        O.trace_generic(fields, c.L, n, c.tau, X, V, half)
+        assert np.array_equal(X, z[kx]) and np.array_equal(V, z[kv])
+    Xu, Vu = z["x"].copy(), z["v"].copy()
+    O.trace_generic({k: ("uniform", z["E_uniform"]) for k in range(n + 1)}, c.L, n, c.tau, Xu, Vu, True)
+    assert np.array_equal(Xu, z["X_uniform"]) and np.array_equal(Vu, z["V_uniform"])
