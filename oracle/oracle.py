@@ -207,7 +207,12 @@ def _lib():
 
 
 def max_threads() -> int:
-    return int(_lib().oracle_max_threads())
+    """Every host thread this process may run on (not OMP_NUM_THREADS: torchrun sets it to 1
+    for each rank, and the CPU baseline should use the whole host)."""
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except (AttributeError, OSError):  # pragma: no cover - non-Linux
+        return max(1, os.cpu_count() or int(_lib().oracle_max_threads()))
 
 
 def trace_backward(coeffs, L, n, tau, X, V, half_kick, threads=0) -> int:
