@@ -1324,13 +1324,24 @@ int nufi_trace(nufi_handle *h, int64_t n, double *X, double *V, int64_t M, int h
     if (M == 0) return NUFI_OK;  // kernels.py:403-404
     if (!X || !V) return fail(NUFI_ERR_USAGE, "null points");
     const size_t bytes = (size_t)M * h->d * sizeof(double);
-    double *dX = X, *dV = V;
+    double *dX = X, *dV = V, *dovr = nullptr;
     const bool dx = is_device_ptr(X), dv = is_device_ptr(V);
+    // stream-ordered staging buffers, released on every exit path
+    struct Staging {
+        cudaStream_t st;
+        double **p[3];
+        bool own[3];
+        ~Staging() {
+            for (int i = 0; i < 3; ++i)
+                if (own[i] && *p[i]) cudaFreeAsync(*p[i], st);
+        }
+    } staging{h->stream, {&dX, &dV, &dovr}, {!dx, !dv, true}};
+    if (!dx) dX = nullptr;
+    if (!dv) dV = nullptr;
     if (!dx) CU(cudaMallocAsync(&dX, bytes, h->stream));
     if (!dv) CU(cudaMallocAsync(&dV, bytes, h->stream));
     if (!dx) CU(cudaMemcpyAsync(dX, X, bytes, cudaMemcpyHostToDevice, h->stream));
     if (!dv) CU(cudaMemcpyAsync(dV, V, bytes, cudaMemcpyHostToDevice, h->stream));
-    double *dovr = nullptr;
     if (h->n_ovr > 0) {
         // the reference's generic path (flow.py:65-82): every slot through its field object
         std::vector<double> tab(4 * (size_t)(n + 1), 0.0);
@@ -1339,15 +1350,12 @@ int nufi_trace(nufi_handle *h, int64_t n, double *X, double *V, int64_t M, int h
         CU(cudaMemcpyAsync(dovr, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, h->stream));
         CU(launch_trace_points_generic(h->d, h->hist, h->nodes, dovr, h->N, h->cfg.L, (int)n, h->cfg.tau, dX, dV, M,
                                        half_kick ? 1 : 0, h->stream));
-        CU(cudaFreeAsync(dovr, h->stream));
     } else {
         CU(launch_trace_points(h->d, mode, h->pow2, h->hist, h->ev_hist, h->ev_elems, h->N, h->nodes, h->cfg.L,
                                (int)n, h->cfg.tau, h->K, dX, dV, M, half_kick ? 1 : 0, h->stream));
     }
     if (!dx) CU(cudaMemcpyAsync(X, dX, bytes, cudaMemcpyDeviceToHost, h->stream));
     if (!dv) CU(cudaMemcpyAsync(V, dV, bytes, cudaMemcpyDeviceToHost, h->stream));
-    if (!dx) CU(cudaFreeAsync(dX, h->stream));
-    if (!dv) CU(cudaFreeAsync(dV, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     if (evals) *evals += M * need;
     return NUFI_OK;
