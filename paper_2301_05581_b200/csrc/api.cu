@@ -79,6 +79,24 @@ static int fail(int code, const std::string &msg) {
             return fail(NUFI_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));     \
     } while (0)
 
+// Stream-ordered temporary device buffers of one call, released on every exit path
+// (including the early returns of CU).
+struct AsyncTemps {
+    cudaStream_t st;
+    void *p[4] = {nullptr, nullptr, nullptr, nullptr};
+    int n = 0;
+    explicit AsyncTemps(cudaStream_t s) : st(s) {}
+    template <class T>
+    cudaError_t alloc(T **out, size_t bytes) {
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(out), bytes, st);
+        if (e == cudaSuccess) p[n++] = *out;
+        return e;
+    }
+    ~AsyncTemps() {
+        for (int i = 0; i < n; ++i) cudaFreeAsync(p[i], st);
+    }
+};
+
 #define CHECK_HANDLE(h)                                                                           \
     do {                                                                                          \
         if (!(h)) return fail(NUFI_ERR_USAGE, "null handle");                                     \
@@ -1326,27 +1344,16 @@ int nufi_trace(nufi_handle *h, int64_t n, double *X, double *V, int64_t M, int h
     const size_t bytes = (size_t)M * h->d * sizeof(double);
     double *dX = X, *dV = V, *dovr = nullptr;
     const bool dx = is_device_ptr(X), dv = is_device_ptr(V);
-    // stream-ordered staging buffers, released on every exit path
-    struct Staging {
-        cudaStream_t st;
-        double **p[3];
-        bool own[3];
-        ~Staging() {
-            for (int i = 0; i < 3; ++i)
-                if (own[i] && *p[i]) cudaFreeAsync(*p[i], st);
-        }
-    } staging{h->stream, {&dX, &dV, &dovr}, {!dx, !dv, true}};
-    if (!dx) dX = nullptr;
-    if (!dv) dV = nullptr;
-    if (!dx) CU(cudaMallocAsync(&dX, bytes, h->stream));
-    if (!dv) CU(cudaMallocAsync(&dV, bytes, h->stream));
+    AsyncTemps tmp(h->stream);
+    if (!dx) CU(tmp.alloc(&dX, bytes));
+    if (!dv) CU(tmp.alloc(&dV, bytes));
     if (!dx) CU(cudaMemcpyAsync(dX, X, bytes, cudaMemcpyHostToDevice, h->stream));
     if (!dv) CU(cudaMemcpyAsync(dV, V, bytes, cudaMemcpyHostToDevice, h->stream));
     if (h->n_ovr > 0) {
         // the reference's generic path (flow.py:65-82): every slot through its field object
         std::vector<double> tab(4 * (size_t)(n + 1), 0.0);
         std::copy(h->ovr.begin(), h->ovr.begin() + std::min(h->ovr.size(), tab.size()), tab.begin());
-        CU(cudaMallocAsync(&dovr, tab.size() * sizeof(double), h->stream));
+        CU(tmp.alloc(&dovr, tab.size() * sizeof(double)));
         CU(cudaMemcpyAsync(dovr, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, h->stream));
         CU(launch_trace_points_generic(h->d, h->hist, h->nodes, dovr, h->N, h->cfg.L, (int)n, h->cfg.tau, dX, dV, M,
                                        half_kick ? 1 : 0, h->stream));
@@ -1422,24 +1429,23 @@ int nufi_eval_field(nufi_handle *h, int64_t slot, const double *X, int64_t M, do
     const size_t bytes = (size_t)M * h->d * sizeof(double);
     const double *dX = X;
     double *tX = nullptr, *dphi = phi_out, *dE = E_out, *tphi = nullptr, *tE = nullptr;
+    AsyncTemps tmp(h->stream);
     if (!is_device_ptr(X)) {
-        CU(cudaMallocAsync(&tX, bytes, h->stream));
+        CU(tmp.alloc(&tX, bytes));
         CU(cudaMemcpyAsync(tX, X, bytes, cudaMemcpyHostToDevice, h->stream));
         dX = tX;
     }
     if (phi_out && !is_device_ptr(phi_out)) {
-        CU(cudaMallocAsync(&tphi, (size_t)M * sizeof(double), h->stream));
+        CU(tmp.alloc(&tphi, (size_t)M * sizeof(double)));
         dphi = tphi;
     }
     if (E_out && !is_device_ptr(E_out)) {
-        CU(cudaMallocAsync(&tE, bytes, h->stream));
+        CU(tmp.alloc(&tE, bytes));
         dE = tE;
     }
     CU(launch_eval_field(h->d, h->hist + (size_t)slot * h->nodes, h->N, h->cfg.L, dX, M, dphi, dE, h->stream));
     if (tphi) CU(cudaMemcpyAsync(phi_out, tphi, (size_t)M * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     if (tE) CU(cudaMemcpyAsync(E_out, tE, bytes, cudaMemcpyDeviceToHost, h->stream));
-    for (void *q : {(void *)tX, (void *)tphi, (void *)tE})
-        if (q) CU(cudaFreeAsync(q, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     return NUFI_OK;
 }
@@ -1452,7 +1458,8 @@ static int poisson_fit(nufi_handle *h, int mode, const double *in, double *out, 
     const size_t bytes = (size_t)h->nodes * sizeof(double);
     // device staging: in, out, spec re / im, W (one allocation)
     double *buf = nullptr;
-    CU(cudaMallocAsync(&buf, 4 * bytes + 64, h->stream));
+    AsyncTemps tmp(h->stream);
+    CU(tmp.alloc(&buf, 4 * bytes + 64));
     double *din = buf, *dout = buf + h->nodes, *dre = buf + 2 * h->nodes, *dim = buf + 3 * h->nodes,
            *dW = buf + 4 * h->nodes;
     CU(cudaMemcpyAsync(din, in, bytes, cudaMemcpyDefault, h->stream));
@@ -1465,7 +1472,6 @@ static int poisson_fit(nufi_handle *h, int mode, const double *in, double *out, 
     if (spec_re) CU(cudaMemcpyAsync(spec_re, dre, bytes, cudaMemcpyDefault, h->stream));
     if (spec_im) CU(cudaMemcpyAsync(spec_im, dim, bytes, cudaMemcpyDefault, h->stream));
     if (W_out) CU(cudaMemcpyAsync(W_out, dW, sizeof(double), cudaMemcpyDefault, h->stream));
-    CU(cudaFreeAsync(buf, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     if (st == NUFI_ERR_NUMERICAL) {
         CU(cudaMemsetAsync(h->d_status, 0, sizeof(int), h->stream));
@@ -1492,26 +1498,24 @@ int nufi_eval_f0(nufi_handle *h, const double *X, const double *V, int64_t M, do
     const double *dX = X, *dV = V;
     double *dF = F;
     double *tX = nullptr, *tV = nullptr, *tF = nullptr;
+    AsyncTemps tmp(h->stream);
     if (!is_device_ptr(X)) {
-        CU(cudaMallocAsync(&tX, bytes, h->stream));
+        CU(tmp.alloc(&tX, bytes));
         CU(cudaMemcpyAsync(tX, X, bytes, cudaMemcpyHostToDevice, h->stream));
         dX = tX;
     }
     if (!is_device_ptr(V)) {
-        CU(cudaMallocAsync(&tV, bytes, h->stream));
+        CU(tmp.alloc(&tV, bytes));
         CU(cudaMemcpyAsync(tV, V, bytes, cudaMemcpyHostToDevice, h->stream));
         dV = tV;
     }
     const bool df = is_device_ptr(F);
     if (!df) {
-        CU(cudaMallocAsync(&tF, M * sizeof(double), h->stream));
+        CU(tmp.alloc(&tF, M * sizeof(double)));
         dF = tF;
     }
     CU(launch_eval_f0(h->d, h->f0, dX, dV, M, dF, h->stream));
     if (!df) CU(cudaMemcpyAsync(F, dF, M * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-    if (tX) CU(cudaFreeAsync(tX, h->stream));
-    if (tV) CU(cudaFreeAsync(tV, h->stream));
-    if (tF) CU(cudaFreeAsync(tF, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     return NUFI_OK;
 }
