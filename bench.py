@@ -265,6 +265,7 @@ def gpu_arm(args, rank: int, world: int):
     # ---- e2e: the public API with host outputs (per-step D2H inside the timed region) ----
     e2e_times = []
     d2h = steps_per_run * (g.n_nodes * (1 + g.d) + 4) * 8
+    h2d = ctypes.sizeof(_lib.NufiConfig)  # the run's configuration descriptor (nufi_create)
     if not dist_mode:
         for i in range(args.warmup + args.steps):
             torch.cuda.synchronize()
@@ -338,8 +339,11 @@ def gpu_arm(args, rank: int, world: int):
                        "point_steps_per_run": ps_run, "l2": "flushed (256 MiB write) between timed runs",
                        "parallelism": f"v-block sharding x{world}" if dist_mode else "single GPU"},
             "wall_s_to_t_end": ms_per_run / 1e3,
-            "e2e": {"value": e2e_value, "unit": "point-steps/s", "h2d_bytes_per_step": 0,
+            "e2e": {"value": e2e_value, "unit": "point-steps/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
+                    "inputs": "a run's only input is its nufi_config descriptor (host struct, copied into the "
+                              "handle and kernel parameters inside the timed region); NuFI keeps no per-point "
+                              "state, and every per-time-step output row (rho, E, W, stats) is copied back",
                     "api": ("Simulation(grid, ic, tau, N).run()" if not dist_mode else
                             "DistributedSimulation(grid, ic, tau, N).run() on every rank (max over ranks)")
                            + " -> host numpy rho/E/W/stats per time step"},
