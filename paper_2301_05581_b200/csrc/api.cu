@@ -27,6 +27,9 @@ cudaError_t launch_sweep_moments(int d, int ppt, bool pow2, const TraceRhoParams
 cudaError_t launch_reduce_moments(const double *part, int rows, int d, double measure, double *out, cudaStream_t st);
 cudaError_t launch_reduce_blocks(const double *partial, const double *fminmax, double *out, int nodes,
                                  int node_tiles, int vt_per_block, int b_lo, int b_hi, int B, cudaStream_t st);
+cudaError_t launch_trace_points_ring(int d, bool pow2, const double *ev_hist, int ev_slab_elems, int N, double L,
+                                     int n, double tau, double K, double *X, double *V, int64_t M, int half_kick,
+                                     cudaStream_t st);
 cudaError_t launch_trace_points_generic(int d, const double *hist, int nodes, const double *ovr, int N, double L,
                                         int n, double tau, double *X, double *V, int64_t M, int half_kick,
                                         cudaStream_t st);
@@ -1358,8 +1361,15 @@ int nufi_trace(nufi_handle *h, int64_t n, double *X, double *V, int64_t M, int h
         CU(launch_trace_points_generic(h->d, h->hist, h->nodes, dovr, h->N, h->cfg.L, (int)n, h->cfg.tau, dX, dV, M,
                                        half_kick ? 1 : 0, h->stream));
     } else {
-        CU(launch_trace_points(h->d, mode, h->pow2, h->hist, h->ev_hist, h->ev_elems, h->N, h->nodes, h->cfg.L,
-                               (int)n, h->cfg.tau, h->K, dX, dV, M, half_kick ? 1 : 0, h->stream));
+        cudaError_t e = cudaErrorNotSupported;
+        // d >= 2: slabs staged in a shared-memory ring (NUFI_TP_NORING=1: the in-place kernel, for tests)
+        if (mode == NUFI_TRACE_FAST && !h->gl && !getenv("NUFI_TP_NORING"))
+            e = launch_trace_points_ring(h->d, h->pow2, h->ev_hist, h->ev_elems, h->N, h->cfg.L, (int)n, h->cfg.tau,
+                                         h->K, dX, dV, M, half_kick ? 1 : 0, h->stream);
+        if (e == cudaErrorNotSupported)
+            e = launch_trace_points(h->d, mode, h->pow2, h->hist, h->ev_hist, h->ev_elems, h->N, h->nodes, h->cfg.L,
+                                    (int)n, h->cfg.tau, h->K, dX, dV, M, half_kick ? 1 : 0, h->stream);
+        CU(e);
     }
     if (!dx) CU(cudaMemcpyAsync(X, dX, bytes, cudaMemcpyDeviceToHost, h->stream));
     if (!dv) CU(cudaMemcpyAsync(V, dV, bytes, cudaMemcpyDeviceToHost, h->stream));

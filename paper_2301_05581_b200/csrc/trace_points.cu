@@ -8,6 +8,9 @@
 //          as written, contraction order m -> q -> w, no FMA contraction:
 //          __dmul_rn / __dadd_rn), reading the raw coefficient history.  It
 //          reproduces the numba kernels' X, V bit for bit.
+#include <algorithm>
+#include <cstdlib>
+
 #include "trace_common.cuh"
 
 namespace nufi {
@@ -191,6 +194,89 @@ __global__ void trace_points_fast(const double *__restrict__ ev_hist, int ev_sla
     }
 }
 
+// Production arithmetic on caller points with the evaluation slabs staged in a shared-memory
+// TMA ring (d >= 2), as in the density kernel: the CTA's 32 * warps * PPT points (PPT
+// interleaved per thread) of each pass share one backward stream of slabs n-1 .. 0, instead
+// of every thread gathering from L1/L2 (random caller points keep little slab locality
+// there).  The optional leading half kick reads slab n in place.  Same substep arithmetic
+// as trace_points_fast, so the two agree bit for bit.
+template <int D, int PPT, bool POW2, int NX>
+__global__ void __launch_bounds__(256, 2)
+    trace_points_ring(const double *__restrict__ ev_hist, int slab_elems, int N_, double inv_h, double tau, double K,
+                      int n, double *X, double *V, int64_t M, int half_kick, int passes, int sps, int stages) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int N = NX ? NX : N_;
+    const int warps = blockDim.x >> 5, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double *ring = reinterpret_cast<double *>(smem_raw);
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)stages * sps * slab_elems);
+    uint64_t *empty = full + stages;
+    const int stages_per_pass = (n + sps - 1) / sps;
+    const int total_it = passes * stages_per_pass;
+    auto issue = [&](int it) {
+        const int st = it % stages_per_pass, s = it % stages;
+        const int k_hi = n - 1 - st * sps, k_lo = max(0, k_hi - sps + 1);
+        const uint32_t bytes = (uint32_t)((k_hi - k_lo + 1) * slab_elems * sizeof(double));
+        mbar_arrive_expect_tx(&full[s], bytes);
+        tma_bulk_g2s(ring + (size_t)s * sps * slab_elems, ev_hist + (size_t)k_lo * slab_elems, bytes, &full[s]);
+    };
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], warps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int it = 0; it < min(stages, total_it); ++it) issue(it);
+    const double s_in = tau * inv_h, s_out = 1.0 / s_in, hx = 1.0 / inv_h;
+    const int64_t per_pass = (int64_t)32 * warps * PPT;
+    int it = 0;
+    for (int pass = 0; pass < passes; ++pass) {
+        const int64_t base = ((int64_t)blockIdx.x * passes + pass) * per_pass + (int64_t)warp * PPT * 32 + lane;
+        double Xs[PPT][D], Vs[PPT][D];
+#pragma unroll
+        for (int pp = 0; pp < PPT; ++pp) {
+            const int64_t q = base + pp * 32;
+            const int64_t qq = q < M ? q : M - 1;  // the tail CTA's spare lanes trace a copy, never stored
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                Xs[pp][a] = fma(X[qq * D + a], inv_h, -0.5);
+                Vs[pp][a] = V[qq * D + a] * s_in;
+            }
+            if (half_kick) kick<D, POW2, NX>(Xs[pp], Vs[pp], ev_hist + (size_t)n * slab_elems, N, K, true);
+        }
+        for (int st = 0; st < stages_per_pass; ++st, ++it) {
+            const int s = it % stages;
+            const uint32_t u = (uint32_t)(it / stages);
+            const int k_hi = n - 1 - st * sps, k_lo = max(0, k_hi - sps + 1);
+            mbar_wait(&full[s], u & 1u);
+            const double *buf = ring + (size_t)s * sps * slab_elems;
+            for (int k = k_hi; k >= k_lo; --k) {
+                const double *slab = buf + (size_t)(k - k_lo) * slab_elems;
+#pragma unroll
+                for (int pp = 0; pp < PPT; ++pp) substep<D, POW2, NX>(Xs[pp], Vs[pp], slab, N, K, false);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if (threadIdx.x == 0 && it + stages < total_it) {
+                mbar_wait(&empty[s], u & 1u);
+                issue(it + stages);
+            }
+        }
+#pragma unroll
+        for (int pp = 0; pp < PPT; ++pp) {
+            const int64_t q = base + pp * 32;
+            if (q < M)
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    X[q * D + a] = (Xs[pp][a] + 0.5) * hx;
+                    V[q * D + a] = Vs[pp][a] * s_out;
+                }
+        }
+    }
+}
+
 // SplineField.eval_phi_many / eval_E_many (spline.py:46-52 -> kernels.py:84-123, the numpy
 // twin): _locate (np.mod, u >= L -> 0), bspline_weights / dweights, the 4^d stencil in
 // itertools.product order (x tap slowest), phi += c * prod w, E_g -= c * prod (dw on axis
@@ -368,6 +454,43 @@ cudaError_t launch_trace_points_generic(int d, const double *hist, int nodes, co
     if (d == 2) trace_points_generic<2><<<ctas, threads, 0, st>>>(hist, nodes, ovr, N, L, n, tau, X, V, M, half_kick);
     if (d == 3) trace_points_generic<3><<<ctas, threads, 0, st>>>(hist, nodes, ovr, N, L, n, tau, X, V, M, half_kick);
     return cudaGetLastError();
+}
+
+// d >= 2 FAST trace on caller points through a staged slab ring (trace_points_ring);
+// returns cudaErrorNotSupported when the ring would not fit (the caller then uses the
+// in-place kernel).
+cudaError_t launch_trace_points_ring(int d, bool pow2, const double *ev_hist, int ev_slab_elems, int N, double L,
+                                     int n, double tau, double K, double *X, double *V, int64_t M, int half_kick,
+                                     cudaStream_t st) {
+    if (d < 2 || n < 1) return cudaErrorNotSupported;
+    const int threads = 256, ppt = 2, warps = threads / 32;
+    const size_t slab_bytes = (size_t)ev_slab_elems * sizeof(double);
+    const int sps = std::max<int>(1, (int)(40960 / slab_bytes)), stages = 2;
+    const size_t smem = (size_t)stages * sps * slab_bytes + 2 * stages * sizeof(uint64_t);
+    if (smem > 110 * 1024) return cudaErrorNotSupported;  // two CTAs per SM, as the density kernel
+    const int64_t per_cta_pass = (int64_t)32 * warps * ppt;
+    const int64_t chunks = (M + per_cta_pass - 1) / per_cta_pass;
+    const int passes = chunks >= 4 * 296 ? 4 : (chunks >= 2 * 296 ? 2 : 1);  // amortise the stream
+    const int ctas = (int)((chunks + passes - 1) / passes);
+    const double inv_h = (double)N / L;
+#define NUFI_TPR(DD, NN, P2)                                                                                 \
+    {                                                                                                        \
+        auto kern = trace_points_ring<DD, 2, P2, NN>;                                                        \
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+        if (e != cudaSuccess) return e;                                                                      \
+        kern<<<ctas, threads, smem, st>>>(ev_hist, ev_slab_elems, N, inv_h, tau, K, n, X, V, M, half_kick,  \
+                                          passes, sps, stages);                                              \
+        return cudaGetLastError();                                                                           \
+    }
+    if (d == 2) {
+        if (N == 32) NUFI_TPR(2, 32, true)
+        if (pow2) NUFI_TPR(2, 0, true)
+        NUFI_TPR(2, 0, false)
+    }
+    if (N == 16) NUFI_TPR(3, 16, true)
+    if (pow2) NUFI_TPR(3, 0, true)
+    NUFI_TPR(3, 0, false)
+#undef NUFI_TPR
 }
 
 cudaError_t launch_eval_f0(int d, const F0Params &f0, const double *X, const double *V, int64_t M, double *F,

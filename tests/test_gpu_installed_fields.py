@@ -122,3 +122,22 @@ def test_install_field_matches_reference_goldens(base):
         ctx_u.install_field(k, nufi.UniformField(z["E_uniform"]))
     X, V = psi_batch(ctx_u, n, z["x"], z["v"])
     assert np.array_equal(X, z["X_uniform"]) and np.array_equal(V, z["V_uniform"])
+
+
+@pytest.mark.parametrize("d,Nx,n,M", [(2, 32, 30, 20000), (2, 6, 9, 3000), (3, 16, 12, 9000), (3, 5, 7, 1500)])
+def test_staged_point_trace_matches_in_place_kernel(d, Nx, n, M, monkeypatch):
+    """FAST point traces for d >= 2 run through a shared-memory slab ring (trace_points_ring);
+    the in-place kernel (NUFI_TP_NORING) computes the same arithmetic: bit-identical, incl.
+    partial last CTAs, multi-pass CTAs and non-power-of-two grids."""
+    ctx, grid = _ctx(d, Nx=Nx, cap=n + 2)
+    rng = np.random.default_rng(40 + d + Nx)
+    ctx.history.load_stack(rng.normal(0.0, 0.2, (n + 1,) + grid.shape_x))
+    x = rng.uniform(-grid.L, 2 * grid.L, (M, d))
+    v = rng.uniform(-5.0, 5.0, (M, d))
+    for half in (True, False):
+        fn = psi_batch if half else psi_tilde_batch
+        X1, V1 = fn(ctx, n, x, v)
+        monkeypatch.setenv("NUFI_TP_NORING", "1")
+        X0, V0 = fn(ctx, n, x, v)
+        monkeypatch.delenv("NUFI_TP_NORING")
+        assert np.array_equal(X1, X0) and np.array_equal(V1, V0)
