@@ -159,6 +159,16 @@ int nufi_mg_setup(nufi_handle *h, int world, int rank, int emulate, void *ipc_ha
 int nufi_mg_connect(nufi_handle *h, const void *ipc_handles);
 int nufi_mg_handle_size(void);
 
+/* Multi-rank d = 2, 3 step with the exchange FUSED into the block reduce (no NCCL):
+ * after nufi_mg_setup / nufi_mg_connect on a d >= 2 handle, one call enqueues step n
+ * (n == history length): trace of this rank's blocks -> block sums STORED into every
+ * rank's exchange table over peer memory + system-scope arrival counters -> the step
+ * tail, which waits for every peer's counters (4 s watchdog: NUFI_ERR_COMM from
+ * nufi_check_status).  Outputs are device buffers (any may be NULL); no host sync.
+ * Emulated handles (emulate != 0) run every virtual rank's exchange on this device. */
+int nufi_mg_step_async(nufi_handle *h, int64_t n, double *rho_out, double *E_out, double *W_out,
+                       double *stats3);
+
 /* Fixed-order combine of the (allreduced) block partials -> rho, stats3. */
 int nufi_rho_finish(nufi_handle *h, const double *partials, double *rho_out, double *stats3);
 int64_t nufi_partials_len(nufi_handle *h); /* v_blocks * (Nx^d + 2) */

@@ -95,6 +95,7 @@ _SIGS = {
     "nufi_mg_setup": [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P],
     "nufi_mg_connect": [_P, _P],
     "nufi_mg_handle_size": [],
+    "nufi_mg_step_async": [_P, _I64, _P, _P, _P, _P],
     "nufi_partials_len": [_P],
     "nufi_field_update": [_P, _P, _P, _P, _P],
     "nufi_step": [_P, _I64, _P, _P, _P, _P, _I64P],

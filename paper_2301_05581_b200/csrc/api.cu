@@ -25,6 +25,8 @@ cudaError_t launch_trace_rho(int d, int ppt, bool pow2, const TraceRhoParams &p,
 cudaError_t launch_sweep_moments(int d, int ppt, bool pow2, const TraceRhoParams &p, double K, int ctas, int threads,
                                  cudaStream_t st);
 cudaError_t launch_reduce_moments(const double *part, int rows, int d, double measure, double *out, cudaStream_t st);
+int launch_reduce_exchange(const double *partial, const double *fminmax, int nodes, int node_tiles, int vt_per_block,
+                           int b_lo, int b_hi, int B, const MgExchange &x, cudaStream_t st);
 cudaError_t launch_reduce_blocks(const double *partial, const double *fminmax, double *out, int nodes,
                                  int node_tiles, int vt_per_block, int b_lo, int b_hi, int B, cudaStream_t st);
 cudaError_t launch_trace_points_ring(int d, bool pow2, const double *ev_hist, int ev_slab_elems, int N, double L,
@@ -1048,6 +1050,11 @@ int nufi_check_status(nufi_handle *h) {
         CU(cudaMemsetAsync(h->d_status, 0, sizeof(int), h->stream));
         return fail(NUFI_ERR_NUMERICAL, "solve_poisson: density is not neutral: nodal mean exceeds 1e-8 max|rho|");
     }
+    if (st == NUFI_ERR_COMM) {
+        h->len = dlen;
+        CU(cudaMemsetAsync(h->d_status, 0, sizeof(int), h->stream));
+        return fail(NUFI_ERR_COMM, "multi-rank step: a peer rank did not arrive within 4 s (watchdog)");
+    }
     return NUFI_OK;
 }
 
@@ -1064,8 +1071,8 @@ static unsigned *mg_flags(const nufi_handle *h, void *buf) {
 
 int nufi_mg_setup(nufi_handle *h, int world, int rank, int emulate, void *ipc_handle_out) {
     CHECK_HANDLE(h);
-    if (h->d != 1 || h->large)
-        return fail(NUFI_ERR_USAGE, "the fused multi-rank run is the d = 1 persistent kernel (Nx <= 4096)");
+    if (h->large)
+        return fail(NUFI_ERR_USAGE, "the fused multi-rank exchange needs the single-CTA step tail (Nx^d <= 4096)");
     if (world < 2 || world > NUFI_MG_MAX || rank < 0 || rank >= world)
         return fail(NUFI_ERR_USAGE, "world must be 2..8 and 0 <= rank < world");
     if (h->B % world) return fail(NUFI_ERR_USAGE, "v_blocks must be a multiple of the rank count");
@@ -1124,6 +1131,69 @@ int nufi_mg_connect(nufi_handle *h, const void *ipc_handles) {
 }
 
 int nufi_mg_handle_size(void) { return (int)sizeof(cudaIpcMemHandle_t); }
+
+// d >= 2 multi-rank step with the exchange fused into the block reduce (no NCCL):
+// trace this rank's blocks -> reduce_exchange (block sums stored into every rank's table
+// over peer memory + arrival counters) -> field update waiting on the counters.  Emulated
+// mode (one GPU): all blocks traced, then one reduce_exchange per virtual rank (each
+// writing every virtual rank's table), then rank 0's field update -- the same kernels and
+// the same table contents as a real run.  Stream-ordered, device outputs, no host sync;
+// nufi_check_status reports a peer that never arrived (NUFI_ERR_COMM).
+int nufi_mg_step_async(nufi_handle *h, int64_t n, double *rho_out, double *E_out, double *W_out, double *stats3) {
+    CHECK_HANDLE(h);
+    if (!h->mg_own || h->d == 1) return fail(NUFI_ERR_USAGE, "call nufi_mg_setup on a d >= 2 handle first");
+    if (!h->mg_emulated) {
+        for (int q = 0; q < h->mg_world; ++q)
+            if (!h->mg_peer[q]) return fail(NUFI_ERR_USAGE, "call nufi_mg_connect first");
+    }
+    if (int rc = refuse_installed(h)) return rc;
+    if (n != h->len) return fail(NUFI_ERR_USAGE, "mg_step requires len == n");
+    if (n >= h->cap) return fail(NUFI_ERR_USAGE, "history is full (capacity n_max + 1)");
+    for (const void *q : {(const void *)rho_out, (const void *)E_out, (const void *)W_out, (const void *)stats3})
+        if (q && !is_device_ptr(q)) return fail(NUFI_ERR_USAGE, "async step outputs must be device buffers");
+    const int G = h->mg_world, nb = h->B / G;
+    const size_t xoff = (size_t)(h->mg_steps & 1u) * mg_xstride(h);
+    MgExchange x{};
+    x.G = G;
+    for (int q = 0; q < G; ++q) {
+        x.tab[q] = mg_table(h->mg_peer[q]) + xoff;
+        x.flags[q] = mg_flags(h, h->mg_peer[q]);
+    }
+    int rc = enqueue_trace(h, n, h->b_lo, h->b_hi);
+    if (rc) return rc;
+    int ctas = -1;
+    {
+        ProfScope ps(h, 1);
+        for (int r = 0; r < G; ++r) {
+            if (!h->mg_emulated && r != h->mg_rank) continue;
+            x.src = r;
+            ctas = launch_reduce_exchange(h->partial, h->fminmax, h->nodes, h->node_tiles, h->vt_per_block, r * nb,
+                                          (r + 1) * nb, h->B, x, h->stream);
+            if (ctas < 0) return fail(NUFI_ERR_CUDA, "reduce_exchange launch failed");
+        }
+    }
+    FieldParams f = field_params(h);
+    f.sums = x.tab[h->mg_rank];
+    f.rows_per_block = 1;
+    f.minmax = f.sums + (size_t)h->B * h->nodes;
+    f.mm_per_block = 1;
+    f.slot = n;
+    f.rho_out = rho_out;
+    f.stats_out = stats3;
+    f.W_out = W_out;
+    f.E_out = E_out;
+    f.wait_flags = x.flags[h->mg_rank];
+    f.wait_G = G;
+    f.wait_target = (h->mg_steps + 1u) * (unsigned)ctas;  // every rank launches the same CTA count
+    f.wait_error = h->mg_error;
+    {
+        ProfScope ps(h, 2);
+        CU(enqueue_field(h, f));
+    }
+    h->mg_steps += 1;
+    h->len += 1;  // provisional; nufi_check_status() reconciles with the device length
+    return NUFI_OK;
+}
 
 int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, double *W_hist, double *stats_hist,
              int64_t *evals) {

@@ -63,9 +63,18 @@ struct FieldParams {
     // d = 1: shared-memory doubles available beyond field_smem_doubles(N, N, true) for staging
     // the tile-row partials with cp.async (0: read them with register loads)
     int64_t stage_cap;
+    // multi-rank d >= 2 step (nufi_mg_step_async): before reading `sums`, wait until
+    // wait_flags[q] >= wait_target for every source rank q < wait_G (system-scope acquire;
+    // 4 s watchdog -> *wait_error = 1 and NUFI_ERR_COMM in *status, history untouched)
+    const unsigned *wait_flags;
+    int wait_G;
+    unsigned wait_target;
+    int *wait_error;
 };
 
+#ifndef NUFI_MG_MAX
 #define NUFI_MG_MAX 8
+#endif
 
 // d = 1 whole-run persistent kernel (run_1d.cu)
 struct Run1DParams {

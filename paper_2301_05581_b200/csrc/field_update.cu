@@ -15,6 +15,29 @@ __global__ void __launch_bounds__(1024) field_update_kernel(const FieldParams p)
     // an earlier step of an asynchronously enqueued sequence failed (non-neutral rho):
     // leave the history untouched, like the reference which raises before appending
     if (p.status && *(volatile int *)p.status != 0) return;
+    if (p.wait_flags) {
+        __shared__ int failed;
+        if (threadIdx.x == 0) {
+            failed = 0;
+            const unsigned long long t0 = globaltimer_ns();
+            for (int q = 0; q < p.wait_G && !failed; ++q) {
+                unsigned v;
+                for (;;) {
+                    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p.wait_flags + q) : "memory");
+                    if (v >= p.wait_target) break;
+                    if (globaltimer_ns() - t0 > 4000000000ull) {  // 4 s: a peer is gone
+                        failed = 1;
+                        if (p.wait_error) atomicExch(p.wait_error, 1);
+                        if (p.status) atomicExch(p.status, NUFI_ERR_COMM);
+                        break;
+                    }
+                    __nanosleep(NUFI_BARRIER_SLEEP_NS);
+                }
+            }
+        }
+        __syncthreads();
+        if (failed) return;
+    }
     field_update_body(p, fsm);
 }
 

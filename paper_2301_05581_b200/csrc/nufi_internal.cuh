@@ -120,6 +120,23 @@ __device__ __forceinline__ void fence_mbar_init() {
 
 // order this thread's (and, after a CTA barrier, the CTA's) generic-proxy shared-memory
 // accesses before subsequent async-proxy (TMA) accesses of the same bytes
+// multi-rank d >= 2 exchange (reduce_exchange_kernel): this step's parity slot of every
+// rank's table, every rank's arrival counters, and the source slot of the sending rank
+#ifndef NUFI_MG_MAX
+#define NUFI_MG_MAX 8
+#endif
+struct MgExchange {
+    double *tab[NUFI_MG_MAX];
+    unsigned *flags[NUFI_MG_MAX];
+    int G, src;
+};
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // cp.async (Ampere-style LDGSTS): a 16-byte global -> shared copy, L2 only (.cg), that
 // holds no registers while in flight; cp_async_wait_all waits for this thread's copies
 __device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {

@@ -297,6 +297,65 @@ __global__ void reduce_blocks_kernel(const double *__restrict__ partial, const d
     }
 }
 
+// Multi-rank d >= 2: the block reduce of this rank's blocks fused with the exchange --
+// every block sum and block (min, max) is STORED into every rank's exchange table (peer
+// memory over NVLink, CUDA IPC; the same fixed order as reduce_blocks_kernel), then each
+// CTA makes its stores visible with one cumulative system-scope fence and adds 1 to slot
+// `src` of every rank's arrival counters.  The receiving rank's field update waits for
+// the counters (field_update_kernel) instead of an NCCL allreduce.
+__global__ void reduce_exchange_kernel(const double *__restrict__ partial, const double *__restrict__ fminmax,
+                                       int nodes, int node_tiles, int vt_per_block, int b_lo, int b_hi, int B,
+                                       int sum_ctas, MgExchange x) {
+    if ((int)blockIdx.x < sum_ctas) {
+        const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        const int64_t count = (int64_t)(b_hi - b_lo) * nodes;
+        if (tid < count) {
+            const int b = b_lo + (int)(tid / nodes);
+            const int node = (int)(tid % nodes);
+            const double *src = partial + (size_t)b * vt_per_block * nodes + node;
+            double s = 0.0;
+            for (int t = 0; t < vt_per_block; ++t) s += src[(size_t)t * nodes];
+            for (int r = 0; r < x.G; ++r) x.tab[r][(size_t)b * nodes + node] = s;
+        }
+    } else {
+        const int b = b_lo + (int)blockIdx.x - sum_ctas;
+        double mn = DBL_MAX, mx = -DBL_MAX;
+        const int64_t c0 = (int64_t)b * vt_per_block * node_tiles;
+        const int64_t c1 = c0 + (int64_t)vt_per_block * node_tiles;
+        for (int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+            mn = fmin(mn, fminmax[2 * c]);
+            mx = fmax(mx, fminmax[2 * c + 1]);
+        }
+        __shared__ double smn[32], smx[32];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            smn[threadIdx.x >> 5] = mn;
+            smx[threadIdx.x >> 5] = mx;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+                mn = fmin(mn, smn[w]);
+                mx = fmax(mx, smx[w]);
+            }
+            for (int r = 0; r < x.G; ++r) {
+                x.tab[r][(size_t)B * nodes + 2 * b] = mn;
+                x.tab[r][(size_t)B * nodes + 2 * b + 1] = mx;
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("fence.sc.sys;" ::: "memory");
+        for (int r = 0; r < x.G; ++r)
+            asm volatile("red.relaxed.sys.global.add.u32 [%0], 1;" ::"l"(x.flags[r] + x.src) : "memory");
+    }
+}
+
 // ----------------------------------------------------------------------------
 // host-side launch helpers
 // ----------------------------------------------------------------------------
@@ -404,6 +463,16 @@ __global__ void reduce_moments_kernel(const double *__restrict__ part, int rows,
 cudaError_t launch_reduce_moments(const double *part, int rows, int d, double measure, double *out, cudaStream_t st) {
     reduce_moments_kernel<<<1, 256, 0, st>>>(part, rows, mom_sums(d) + 2, mom_sums(d), measure, out);
     return cudaGetLastError();
+}
+
+int launch_reduce_exchange(const double *partial, const double *fminmax, int nodes, int node_tiles, int vt_per_block,
+                           int b_lo, int b_hi, int B, const MgExchange &x, cudaStream_t st) {
+    const int64_t count = (int64_t)(b_hi - b_lo) * nodes;
+    const int threads = 256;
+    const int sum_ctas = (int)((count + threads - 1) / threads);
+    reduce_exchange_kernel<<<sum_ctas + (b_hi - b_lo), threads, 0, st>>>(partial, fminmax, nodes, node_tiles,
+                                                                         vt_per_block, b_lo, b_hi, B, sum_ctas, x);
+    return cudaGetLastError() == cudaSuccess ? sum_ctas + (b_hi - b_lo) : -1;
 }
 
 cudaError_t launch_reduce_blocks(const double *partial, const double *fminmax, double *out, int nodes,

@@ -99,14 +99,15 @@ class DistributedSimulation:
         self.partials = torch.zeros(n, dtype=torch.float64, device=f"cuda:{device}")
         self.block_lo, self.block_hi = lo, hi
         self.fused = False
-        if grid.d == 1 and self.world > 1 and B % self.world == 0 and os.environ.get("NUFI_MG", "1") != "0":
+        if self.world > 1 and B % self.world == 0 and os.environ.get("NUFI_MG", "1") != "0":
             self._connect_fused(device)
 
     def _connect_fused(self, device: int) -> None:
-        """d = 1: the persistent kernel with the exchange fused in (nufi_mg_*): every rank
-        exports its exchange buffer (CUDA IPC), the handles are all-gathered over the
-        process group, every rank opens its peers'.  Falls back to the per-step NCCL
-        loop (with a warning) if peer memory is unavailable."""
+        """The exchange fused into our own kernels (nufi_mg_*): d = 1 the persistent run
+        kernel, d = 2, 3 the block reduce (nufi_mg_step_async).  Every rank exports its
+        exchange buffer (CUDA IPC), the handles are all-gathered over the process group,
+        every rank opens its peers'.  Falls back to the per-step NCCL loop (with a
+        warning) if peer memory is unavailable or the grid needs the multi-CTA tail."""
         import warnings
 
         h = self.history.handle
@@ -124,6 +125,37 @@ class DistributedSimulation:
         except Exception as exc:  # pragma: no cover - depends on the machine's peer access
             warnings.warn(f"fused multi-rank kernel unavailable ({exc}); using the per-step NCCL loop")
             self.fused = False
+
+    def _run_exchange_steps(self, first: int, outputs: dict, ev) -> None:
+        """d = 2, 3 fused loop: nufi_mg_step_async per step (trace own blocks -> block sums
+        stored into every rank's table over peer memory -> tail waiting on the arrival
+        counters), device outputs, one status check at the end."""
+        t = self.torch
+        g = self.grid
+        h = self.history.handle
+        dev = f"cuda:{self.partials.device.index}"
+        steps = self.n_steps + 1 - first
+        host = {k: v for k, v in outputs.items() if v is not None and not hasattr(v, "data_ptr")}
+        dout = {k: (v if hasattr(v, "data_ptr") else None) for k, v in outputs.items()}
+        shapes = dict(rho=(steps, g.n_nodes), E=(steps, g.n_nodes, g.d), W=(steps,), stats=(steps, 3))
+        for k in host:
+            dout[k] = t.empty(shapes[k], dtype=t.float64, device=dev)
+
+        def row(k, n):
+            a = dout.get(k)
+            if a is None:
+                return None
+            width = int(np.prod(shapes[k][1:])) if len(shapes[k]) > 1 else 1
+            return a.data_ptr() + (n - first) * width * 8
+
+        for n in range(first, self.n_steps + 1):
+            h.call("nufi_mg_step_async", n, row("rho", n), row("E", n), row("W", n), row("stats", n))
+        h.call("nufi_check_status")
+        for k, a in host.items():
+            a[...] = dout[k].cpu().numpy().reshape(a.shape)
+        # this rank traced its share of the blocks: P_rank * sum_n n
+        per_step = g.n_nodes * g.n_cells * (self.block_hi - self.block_lo) // self.B
+        ev.value += per_step * sum(range(first, self.n_steps + 1))
 
     def step(self, outputs: dict | None = None, row: int = 0, sync: bool = True):
         """One step: trace own blocks -> allreduce -> redundant field update."""
@@ -170,9 +202,12 @@ class DistributedSimulation:
             ev = ctypes.c_int64(0)
             err = None
             try:
-                self.history.handle.call("nufi_run", self.n_steps, _lib.ptr(outputs.get("rho")),
-                                         _lib.ptr(outputs.get("E")), _lib.ptr(outputs.get("W")),
-                                         _lib.ptr(outputs.get("stats")), ctypes.byref(ev))
+                if g.d == 1:
+                    self.history.handle.call("nufi_run", self.n_steps, _lib.ptr(outputs.get("rho")),
+                                             _lib.ptr(outputs.get("E")), _lib.ptr(outputs.get("W")),
+                                             _lib.ptr(outputs.get("stats")), ctypes.byref(ev))
+                else:
+                    self._run_exchange_steps(first, outputs, ev)
             except NumericalConsistencyError:
                 raise  # the physics, not the transport: same on every rank
             except Exception as exc:  # a peer timed out (watchdog) or the launch failed
@@ -182,8 +217,10 @@ class DistributedSimulation:
                                      device=self.partials.device)
             self.dist.all_reduce(flag, group=self.group)
             if int(flag.item()) == 0:
-                # nufi_run counts the whole grid; this rank traced its share of the blocks
-                self.ctx.field_evals += int(ev.value) * (self.block_hi - self.block_lo) // self.B
+                if g.d == 1:  # nufi_run counts the whole grid; this rank traced its share of the blocks
+                    self.ctx.field_evals += int(ev.value) * (self.block_hi - self.block_lo) // self.B
+                else:
+                    self.ctx.field_evals += int(ev.value)
                 return outputs
             import warnings
 

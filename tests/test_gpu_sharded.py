@@ -162,4 +162,44 @@ def test_fused_multirank_setup_errors():
     w2 = workload("tiny2")
     h2 = nufi.PotentialHistory(w2.grid, w2.tau, capacity=4, v_blocks=8)
     with pytest.raises(nufi.UsageError):
-        h2.handle.call("nufi_mg_setup", 2, 0, 1, None)  # d = 1 only
+        h2.handle.call("nufi_mg_step_async", 0, None, None, None, None)  # no nufi_mg_setup yet
+    wb = workload("big2")
+    hb = nufi.PotentialHistory(wb.grid, wb.tau, capacity=4, v_blocks=6)
+    with pytest.raises(nufi.UsageError):
+        hb.handle.call("nufi_mg_setup", 2, 0, 1, None)  # grids beyond one CTA's tail
+
+
+@pytest.mark.parametrize("name,N", [("tiny2", 12), ("tiny3", 8), ("rag2", 10), ("wl3r", 6)])
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_fused_exchange_d23_emulated(name, N, world):
+    """d >= 2 steps with the exchange fused into the block reduce (nufi_mg_step_async:
+    block sums stored into every rank's table over peer memory + arrival counters, the
+    step tail waiting on them; no NCCL), `world` ranks emulated on this device: rho, W,
+    E, stats and the history bit-identical to the single-GPU run, over repeated runs."""
+    import torch
+
+    w = workload(name)
+    g = w.grid
+    if (g.n_cells % 8) or (8 % world):
+        pytest.skip("needs 8 velocity blocks divisible by the rank count")
+    ref_sim = nufi.Simulation(g, w.ic, w.tau, N, v_blocks=8)
+    ref = ref_sim.run()
+    sim = nufi.Simulation(g, w.ic, w.tau, N, v_blocks=8)
+    h = sim.history.handle
+    h.call("nufi_mg_setup", world, 0, 1, None)
+    for _ in range(2):  # the arrival counters keep counting across runs
+        sim.history.truncate(0)
+        out = dict(rho=torch.empty((N + 1, g.n_nodes), dtype=torch.float64, device="cuda"),
+                   E=torch.empty((N + 1, g.n_nodes * g.d), dtype=torch.float64, device="cuda"),
+                   W=torch.empty(N + 1, dtype=torch.float64, device="cuda"),
+                   stats=torch.empty((N + 1, 3), dtype=torch.float64, device="cuda"))
+        for n in range(N + 1):
+            h.call("nufi_mg_step_async", n, out["rho"][n].data_ptr(), out["E"][n].data_ptr(),
+                   out["W"][n:].data_ptr(), out["stats"][n].data_ptr())
+        h.call("nufi_check_status")
+        res = {k: v.cpu().numpy() for k, v in out.items()}
+        assert np.array_equal(res["rho"], ref.rho.reshape(N + 1, -1))
+        assert np.array_equal(res["W"], ref.W)
+        assert np.array_equal(res["E"], ref.E.reshape(N + 1, -1))
+        assert np.array_equal(res["stats"], ref.stats)
+        assert np.array_equal(sim.history.stacked(), ref_sim.history.stacked())
