@@ -165,6 +165,22 @@ __device__ __forceinline__ void kick(const double (&X)[D], double (&V)[D], const
     }
 }
 
+// d = 1 substep with the drift folded into the kick (run_1d.cu kick1): on entry X is the
+// already drifted position of this substep, on exit the drifted position of the next one,
+// X - V_new = (X - V) - A - fc (B + fc C): the next cell lookup does not wait for a DADD.
+template <bool POW2, int NX = 0>
+__device__ __forceinline__ void kick1_folded(double &X, double &V, const double *__restrict__ slab, int N_) {
+    const int N = NX ? NX : N_;
+    double fc;
+    const int i = locate_centred<POW2>(X, N, fc);
+    double A, B, C;
+    d1_fetch(slab, i, N, A, B, C);
+    const double XmV = X - V;
+    const double t = fma(fc, C, B);
+    X = fma(-fc, t, XmV - A);
+    V = fma(fc, t, V + A);
+}
+
 // One backward substep: drift x -= tau v, then kick through slab.
 template <int D, bool POW2, int NX = 0>
 __device__ __forceinline__ void substep(double (&X)[D], double (&V)[D], const double *__restrict__ slab,

@@ -127,10 +127,25 @@ __global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams 
             if (!GL) mbar_wait(&full[s], u & 1u);
             const double *buf = GL ? p.ev_hist + (size_t)k_lo * slab_elems : ring + (size_t)s * sps * slab_elems;
             // slab 0 is stored pre-halved (field_common.cuh), so every kick is uniform
-            for (int k = k_hi; k >= k_lo; --k) {
-                const double *slab = buf + (size_t)(k - k_lo) * slab_elems;
+            if constexpr (D == 1) {
+                // drift folded into the kick (X carries the look-ahead drift inside the stream)
+                if (st == 0)
 #pragma unroll
-                for (int pp = 0; pp < PPT; ++pp) substep<D, POW2, NX>(X[pp], V[pp], slab, N, K, false);
+                    for (int pp = 0; pp < PPT; ++pp) X[pp][0] -= V[pp][0];
+                for (int k = k_hi; k >= k_lo; --k) {
+                    const double *slab = buf + (size_t)(k - k_lo) * slab_elems;
+#pragma unroll
+                    for (int pp = 0; pp < PPT; ++pp) kick1_folded<POW2, NX>(X[pp][0], V[pp][0], slab, N);
+                }
+                if (st == stages_per_pass - 1)
+#pragma unroll
+                    for (int pp = 0; pp < PPT; ++pp) X[pp][0] += V[pp][0];
+            } else {
+                for (int k = k_hi; k >= k_lo; --k) {
+                    const double *slab = buf + (size_t)(k - k_lo) * slab_elems;
+#pragma unroll
+                    for (int pp = 0; pp < PPT; ++pp) substep<D, POW2, NX>(X[pp], V[pp], slab, N, K, false);
+                }
             }
             if (!GL) {
                 __syncwarp();
@@ -424,6 +439,10 @@ cudaError_t launch_sweep_moments(int d, int ppt, bool pow2, const TraceRhoParams
         if (p.N == 32) return launch_one<DD, PP, true, 32, true>(p, K, ctas, threads, smem, st);      \
         return pow2 ? launch_one<DD, PP, true, 0, true>(p, K, ctas, threads, smem, st)                \
                     : launch_one<DD, PP, false, 0, true>(p, K, ctas, threads, smem, st);              \
+    }
+    if (d == 1 && ppt == 1) {  // the BASELINE d = 1 grids: compile-time plane offsets in the kick
+        if (p.N == 64) return launch_one<1, 1, true, 64, true>(p, K, ctas, threads, smem, st);
+        if (p.N == 256) return launch_one<1, 1, true, 256, true>(p, K, ctas, threads, smem, st);
     }
     NUFI_SW(1, 1)
     NUFI_SW(2, 1)
