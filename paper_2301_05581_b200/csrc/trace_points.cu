@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(256, 2)
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], warps);
+            reinterpret_cast<unsigned *>(&empty[s])[0] = 0u;  // release counter of stage s
         }
         fence_mbar_init();
     }
@@ -258,10 +258,17 @@ __global__ void __launch_bounds__(256, 2)
                 for (int pp = 0; pp < PPT; ++pp) substep<D, POW2, NX>(Xs[pp], Vs[pp], slab, N, K, false);
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
-            if (threadIdx.x == 0 && it + stages < total_it) {
-                mbar_wait(&empty[s], u & 1u);
-                issue(it + stages);
+            if (lane == 0) {  // the last warp to finish the stage refills it (trace_rho.cu)
+                unsigned *cnt = reinterpret_cast<unsigned *>(&empty[s]);
+                __threadfence_block();
+                if (atomicAdd(cnt, 1u) == (unsigned)warps - 1u) {
+                    *cnt = 0u;
+                    __threadfence_block();
+                    if (it + stages < total_it) {
+                        fence_proxy_async_smem();
+                        issue(it + stages);
+                    }
+                }
             }
         }
 #pragma unroll

@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams 
         if (threadIdx.x == 0) {
             for (int s = 0; s < stages; ++s) {
                 mbar_init(&full[s], 1);
-                mbar_init(&empty[s], warps);
+                reinterpret_cast<unsigned *>(&empty[s])[0] = 0u;  // release counter of stage s
             }
             fence_mbar_init();
         }
@@ -148,11 +148,20 @@ __global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams 
                 }
             }
             if (!GL) {
+                // the LAST warp to finish the stage refills it (no warp waits for the others;
+                // a fixed refilling warp would stall on the slowest one every stage)
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);
-                if (threadIdx.x == 0 && it + stages < total_it) {
-                    mbar_wait(&empty[s], u & 1u);
-                    issue(it + stages);
+                if (lane == 0) {
+                    unsigned *cnt = reinterpret_cast<unsigned *>(&empty[s]);
+                    __threadfence_block();
+                    if (atomicAdd(cnt, 1u) == (unsigned)warps - 1u) {
+                        *cnt = 0u;
+                        __threadfence_block();
+                        if (it + stages < total_it) {
+                            fence_proxy_async_smem();  // generic reads of the stage -> async-proxy refill
+                            issue(it + stages);
+                        }
+                    }
                 }
             }
         }
