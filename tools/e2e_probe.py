@@ -19,7 +19,6 @@ for it in range(5):
     t1 = time.perf_counter()
     res = sim.run()
     t2 = time.perf_counter()
-    del sim, res
-    gc.collect()
+    del sim, res  # refcount drop: nufi_destroy runs here (no gc.collect, like the bench loop)
     t3 = time.perf_counter()
     print(f"{name} it{it}: create {1e3*(t1-t0):.1f} ms  run {1e3*(t2-t1):.1f} ms  destroy {1e3*(t3-t2):.1f} ms", flush=True)
