@@ -1,3 +1,4 @@
+"""Time the d=1 observable sweep (nufi_moments) of ts1 at n = 800: python tools/sweep_probe.py (for ncu -k trace_rho)."""
 import sys, os
 sys.path.insert(0, '/root/repo')
 import torch
