@@ -361,7 +361,9 @@ static void choose_tiling(nufi_handle *h) {
     const int slab_bytes = h->ev_elems * 8;
     if (h->d == 1) {
         h->sps = trace_rho_1d_sps(h->N);  // must match the kernel's template instantiation
-        h->stages = 4;  // 2 CTAs / SM still fit for N = 256 (the tail workspace aliases the ring)
+        // N = 256: 4 stages so 2 CTAs / SM still fit (the tail workspace aliases the ring);
+        // small grids run one CTA per SM and take a deeper ring (ts1 barrier wait -5 %)
+        h->stages = h->N <= 64 ? 6 : 4;
         if (const char *e = getenv("NUFI_D1_STAGES")) h->stages = std::max(2, atoi(e));
     } else if (h->d == 2) {
         h->sps = std::max(1, 40960 / slab_bytes);  // ~40 KB stages, 2-deep ring: 2 CTAs / SM
