@@ -366,7 +366,9 @@ static void choose_tiling(nufi_handle *h) {
         h->stages = h->N <= 64 ? 6 : 4;
         if (const char *e = getenv("NUFI_D1_STAGES")) h->stages = std::max(2, atoi(e));
     } else if (h->d == 2) {
-        h->sps = std::max(1, 40960 / slab_bytes);  // ~40 KB stages, 2-deep ring: 2 CTAs / SM
+        // 2-deep ring with stages as large as two CTAs per SM allow (~100 KB of ring per CTA):
+        // fewer, larger refills (wl2: 5 slabs per stage, +2 % over 4)
+        h->sps = std::max(1, (100 * 1024) / (2 * slab_bytes));
         h->stages = 2;
     } else {
         h->sps = std::max(1, 32768 / slab_bytes);
