@@ -472,6 +472,7 @@ cudaError_t launch_run_1d(const Run1DParams &P, int threads, int device, cudaStr
         case 256:
             if (P.tp.slabs_per_stage == 1) return launch_run<256, 1>(P, threads, device, st, grid_out);
             if (P.tp.slabs_per_stage == 2) return launch_run<256, 2>(P, threads, device, st, grid_out);
+            if (P.tp.slabs_per_stage == 8) return launch_run<256, 8>(P, threads, device, st, grid_out);
             return launch_run<256, 4>(P, threads, device, st, grid_out);
         default: return launch_run<0, 1>(P, threads, device, st, grid_out);
     }

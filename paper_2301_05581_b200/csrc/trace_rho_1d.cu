@@ -196,9 +196,9 @@ int trace_rho_1d_sps(int N) {
     if (N == 256) {
         if (const char *e = getenv("NUFI_D1_SPS")) {
             const int v = atoi(e);
-            if (v == 1 || v == 2 || v == 4) return v;
+            if (v == 1 || v == 2 || v == 4 || v == 8) return v;
         }
-        return 4;
+        return 8;  // 2 stages x 8 slabs: fewer ring hand-offs per substep (sl1 248 -> 218 ms vs 4 x 4)
     }
     return 1;
 }
@@ -223,6 +223,7 @@ cudaError_t launch_trace_rho_1d(const TraceRhoParams &p, const FieldParams &fp, 
         case 256:
             if (p.slabs_per_stage == 1) return launch1<256, 1>(p, fp, fuse, ticket, ctas, threads, smem, st);
             if (p.slabs_per_stage == 2) return launch1<256, 2>(p, fp, fuse, ticket, ctas, threads, smem, st);
+            if (p.slabs_per_stage == 8) return launch1<256, 8>(p, fp, fuse, ticket, ctas, threads, smem, st);
             return launch1<256, 4>(p, fp, fuse, ticket, ctas, threads, smem, st);
         default: return launch1<0, 1>(p, fp, fuse, ticket, ctas, threads, smem, st);
     }
