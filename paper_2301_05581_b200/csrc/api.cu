@@ -363,7 +363,8 @@ static void choose_tiling(nufi_handle *h) {
         h->sps = trace_rho_1d_sps(h->N);  // must match the kernel's template instantiation
         // N = 256: 4 stages so 2 CTAs / SM still fit (the tail workspace aliases the ring);
         // small grids run one CTA per SM and take a deeper ring (ts1 barrier wait -5 %)
-        h->stages = h->N <= 64 ? 6 : (h->sps >= 8 && h->N == 256 ? 2 : 4);
+        // deep stages, few hand-offs: 2 x 64 slabs (N = 64, one CTA / SM), 2 x 8 (N = 256, two CTAs / SM)
+        h->stages = (h->N == 64 && h->sps >= 32) || (h->N == 256 && h->sps >= 8) ? 2 : (h->N <= 64 ? 6 : 4);
         if (const char *e = getenv("NUFI_D1_STAGES")) h->stages = std::max(2, atoi(e));
     } else if (h->d == 2) {
         // 2-deep ring with stages as large as two CTAs per SM allow (~100 KB of ring per CTA):

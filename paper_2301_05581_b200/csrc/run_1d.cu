@@ -467,12 +467,16 @@ static cudaError_t launch_run(const Run1DParams &P, int threads, int device, cud
 cudaError_t launch_run_1d(const Run1DParams &P, int threads, int device, cudaStream_t st, int *grid_out) {
     switch (P.tp.N) {
         case 32: return launch_run<32, 16>(P, threads, device, st, grid_out);
-        case 64: return launch_run<64, 16>(P, threads, device, st, grid_out);
+        case 64:
+            if (P.tp.slabs_per_stage == 32) return launch_run<64, 32>(P, threads, device, st, grid_out);
+            if (P.tp.slabs_per_stage == 64) return launch_run<64, 64>(P, threads, device, st, grid_out);
+            return launch_run<64, 16>(P, threads, device, st, grid_out);
         case 128: return launch_run<128, 8>(P, threads, device, st, grid_out);
         case 256:
             if (P.tp.slabs_per_stage == 1) return launch_run<256, 1>(P, threads, device, st, grid_out);
             if (P.tp.slabs_per_stage == 2) return launch_run<256, 2>(P, threads, device, st, grid_out);
             if (P.tp.slabs_per_stage == 8) return launch_run<256, 8>(P, threads, device, st, grid_out);
+            if (P.tp.slabs_per_stage == 16) return launch_run<256, 16>(P, threads, device, st, grid_out);
             return launch_run<256, 4>(P, threads, device, st, grid_out);
         default: return launch_run<0, 1>(P, threads, device, st, grid_out);
     }

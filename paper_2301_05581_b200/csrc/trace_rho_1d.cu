@@ -191,12 +191,17 @@ size_t trace_rho_1d_smem_bytes(const TraceRhoParams &p, int threads, int nodes) 
 
 // slabs per stage for a given N (must match the template instantiations below)
 int trace_rho_1d_sps(int N) {
-    if (N == 32 || N == 64) return 16;
+    if (N == 64) {
+        if (const char *e = getenv("NUFI_D1_SPS"))
+            if (atoi(e) == 16 || atoi(e) == 32) return atoi(e);
+        return 64;  // 2 stages x 64 slabs (192 KB, one CTA per SM): ts1 87.8 -> 80.9 ms vs 6 x 16
+    }
+    if (N == 32) return 16;
     if (N == 128) return 8;
     if (N == 256) {
         if (const char *e = getenv("NUFI_D1_SPS")) {
             const int v = atoi(e);
-            if (v == 1 || v == 2 || v == 4 || v == 8) return v;
+            if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) return v;
         }
         return 8;  // 2 stages x 8 slabs: fewer ring hand-offs per substep (sl1 248 -> 218 ms vs 4 x 4)
     }
@@ -218,12 +223,16 @@ cudaError_t launch_trace_rho_1d(const TraceRhoParams &p, const FieldParams &fp, 
     const size_t smem = trace_rho_1d_smem_bytes(p, threads, p.nodes);
     switch (p.N) {
         case 32: return launch1<32, 16>(p, fp, fuse, ticket, ctas, threads, smem, st);
-        case 64: return launch1<64, 16>(p, fp, fuse, ticket, ctas, threads, smem, st);
+        case 64:
+            if (p.slabs_per_stage == 32) return launch1<64, 32>(p, fp, fuse, ticket, ctas, threads, smem, st);
+            if (p.slabs_per_stage == 64) return launch1<64, 64>(p, fp, fuse, ticket, ctas, threads, smem, st);
+            return launch1<64, 16>(p, fp, fuse, ticket, ctas, threads, smem, st);
         case 128: return launch1<128, 8>(p, fp, fuse, ticket, ctas, threads, smem, st);
         case 256:
             if (p.slabs_per_stage == 1) return launch1<256, 1>(p, fp, fuse, ticket, ctas, threads, smem, st);
             if (p.slabs_per_stage == 2) return launch1<256, 2>(p, fp, fuse, ticket, ctas, threads, smem, st);
             if (p.slabs_per_stage == 8) return launch1<256, 8>(p, fp, fuse, ticket, ctas, threads, smem, st);
+            if (p.slabs_per_stage == 16) return launch1<256, 16>(p, fp, fuse, ticket, ctas, threads, smem, st);
             return launch1<256, 4>(p, fp, fuse, ticket, ctas, threads, smem, st);
         default: return launch1<0, 1>(p, fp, fuse, ticket, ctas, threads, smem, st);
     }
