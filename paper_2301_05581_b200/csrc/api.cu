@@ -46,7 +46,7 @@ cudaError_t launch_eval_f0(int d, const F0Params &f0, const double *X, const dou
                            cudaStream_t st);
 cudaError_t launch_trace_rho_1d(const TraceRhoParams &p, const FieldParams &fp, int fuse, unsigned *ticket, int ctas,
                                 int threads, cudaStream_t st);
-int trace_rho_1d_sps(int N);
+int trace_rho_1d_sps(int N, bool wide);
 cudaError_t launch_trace_rho_global(int d, bool mom, bool pow2, const TraceRhoParams &p, double K, int ctas,
                                     int threads, cudaStream_t st);
 cudaError_t launch_field_large(const FieldParams &f, double *scratch, cudaStream_t st);
@@ -327,6 +327,15 @@ static void choose_tiling(nufi_handle *h) {
     int warps, ppt, passes;
     if (h->d == 1) {
         warps = 8, ppt = 1, passes = 1;  // trace_rho_1d: one point per thread
+        if (h->N == 256) {
+            // throughput regime (many tiles per SM): one 16-warp CTA per SM sharing one deep
+            // ring (2 x 16 slabs) beats two 8-warp CTAs with 2 x 8 each (sl1 218.7 -> 203 ms)
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+            const int64_t rows = per_block * (h->b_hi - h->b_lo), nt = (h->nodes + 31) / 32;
+            if ((rows / 16) * nt >= 2 * (int64_t)sms) warps = 16;
+        }
+        if (const char *e = getenv("NUFI_D1_WARPS")) warps = atoi(e) >= 16 ? 16 : 8;
     } else if (h->d == 2) {
         warps = 8, ppt = 2, passes = 1;  // 2 interleaved points per thread, 2 CTAs / SM
     } else {
@@ -350,7 +359,7 @@ static void choose_tiling(nufi_handle *h) {
     while (ppt > 1 && (per_block % (warps * ppt) != 0)) ppt >>= 1;
     while (passes > 1 && (per_block % ((int64_t)warps * ppt * passes) != 0)) passes >>= 1;
     if (per_block % ((int64_t)warps * ppt * passes) != 0) warps = ppt = passes = 1;
-    h->threads = h->d == 1 ? 256 : warps * 32;  // d = 1: 8 warp slots (+ producer), `warps` of them trace
+    h->threads = h->d == 1 ? (warps > 8 ? 512 : 256) : warps * 32;  // d = 1: warp slots (+ producer)
     h->ppt = ppt;
     h->passes = passes;
     h->vt_rows = warps * ppt * passes;
@@ -360,7 +369,7 @@ static void choose_tiling(nufi_handle *h) {
     // TMA ring: slabs per stage and stage count
     const int slab_bytes = h->ev_elems * 8;
     if (h->d == 1) {
-        h->sps = trace_rho_1d_sps(h->N);  // must match the kernel's template instantiation
+        h->sps = trace_rho_1d_sps(h->N, h->threads > 256);  // must match the kernel's template instantiation
         // N = 256: 4 stages so 2 CTAs / SM still fit (the tail workspace aliases the ring);
         // small grids run one CTA per SM and take a deeper ring (ts1 barrier wait -5 %)
         // deep stages, few hand-offs: 2 x 64 slabs (N = 64, one CTA / SM), 2 x 8 (N = 256, two CTAs / SM)

@@ -67,8 +67,9 @@ __host__ __device__ inline size_t run_1d_ring_doubles(int stages, int sps, int s
     return ((ring > tail ? ring : tail) + 1) & ~(size_t)1;
 }
 
-template <int NX, int SPS>
-__global__ void __launch_bounds__(288, 2) run_1d_kernel(const Run1DParams P) {
+// WIDE: 16 tracing warps + producer in one CTA per SM (experiment knob NUFI_D1_WARPS=16)
+template <int NX, int SPS, int WIDE = 0>
+__global__ void __launch_bounds__(WIDE ? 544 : 288, WIDE ? 1 : 2) run_1d_kernel(const Run1DParams P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const TraceRhoParams &p = P.tp;
     // warps [0, cw) trace (cw = tile rows), the last warp is the TMA producer, any
@@ -430,9 +431,9 @@ size_t run_1d_smem_bytes(const TraceRhoParams &p, int threads) {
            2 * p.stages * sizeof(uint64_t) + (3 * 32 * (size_t)cw + p.ev_slab_elems) * sizeof(double);
 }
 
-template <int NX, int SPS>
+template <int NX, int SPS, int WIDE = 0>
 static cudaError_t launch_run(const Run1DParams &P, int threads, int device, cudaStream_t st, int *grid_out) {
-    auto kern = run_1d_kernel<NX, SPS>;
+    auto kern = run_1d_kernel<NX, SPS, WIDE>;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     const int G = P.mg_ranks > 1 ? P.mg_ranks : 1;
@@ -476,7 +477,9 @@ cudaError_t launch_run_1d(const Run1DParams &P, int threads, int device, cudaStr
             if (P.tp.slabs_per_stage == 1) return launch_run<256, 1>(P, threads, device, st, grid_out);
             if (P.tp.slabs_per_stage == 2) return launch_run<256, 2>(P, threads, device, st, grid_out);
             if (P.tp.slabs_per_stage == 8) return launch_run<256, 8>(P, threads, device, st, grid_out);
-            if (P.tp.slabs_per_stage == 16) return launch_run<256, 16>(P, threads, device, st, grid_out);
+            if (P.tp.slabs_per_stage == 16)
+                return threads > 288 ? launch_run<256, 16, 1>(P, threads, device, st, grid_out)
+                                     : launch_run<256, 16>(P, threads, device, st, grid_out);
             return launch_run<256, 4>(P, threads, device, st, grid_out);
         default: return launch_run<0, 1>(P, threads, device, st, grid_out);
     }

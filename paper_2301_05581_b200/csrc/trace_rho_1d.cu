@@ -54,7 +54,7 @@ __device__ __forceinline__ void kick1d_any(double &X, double &V, const double *_
 // Block = C consumer warps (one point per thread) + 1 producer warp that keeps
 // the TMA ring full, so no consumer ever waits for a refill it did not need.
 template <int NX, int SPS>
-__global__ void __launch_bounds__(288) trace_rho_1d_kernel(const TraceRhoParams p, const FieldParams fp, int fuse,
+__global__ void __launch_bounds__(544) trace_rho_1d_kernel(const TraceRhoParams p, const FieldParams fp, int fuse,
                                                             unsigned *ticket) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int cw = p.vt_rows;  // tracing warps (tile rows); the last warp is the producer
@@ -190,7 +190,7 @@ size_t trace_rho_1d_smem_bytes(const TraceRhoParams &p, int threads, int nodes) 
 }
 
 // slabs per stage for a given N (must match the template instantiations below)
-int trace_rho_1d_sps(int N) {
+int trace_rho_1d_sps(int N, bool wide) {
     if (N == 64) {
         if (const char *e = getenv("NUFI_D1_SPS"))
             if (atoi(e) == 16 || atoi(e) == 32) return atoi(e);
@@ -203,7 +203,9 @@ int trace_rho_1d_sps(int N) {
             const int v = atoi(e);
             if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) return v;
         }
-        return 8;  // 2 stages x 8 slabs: fewer ring hand-offs per substep (sl1 248 -> 218 ms vs 4 x 4)
+        // 2 stages x 8 slabs for two 8-warp CTAs per SM (sl1 248 -> 218 ms vs 4 x 4), 2 x 16 for
+        // one 16-warp CTA per SM (218 -> 203 ms)
+        return wide ? 16 : 8;
     }
     return 1;
 }
