@@ -135,7 +135,7 @@ def _emulated_mg_run(name, N, world, repeat=1):
     return sim, res
 
 
-@pytest.mark.parametrize("name,N", [("kat_wl", 60), ("ts1", 200), ("rag1", 20)])
+@pytest.mark.parametrize("name,N", [("kat_wl", 60), ("ts1", 200), ("rag1", 20), ("sl1", 24)])
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_fused_multirank_kernel_emulated(name, N, world):
     """The fused multi-rank persistent kernel (exchange over peer memory + arrival flags,
