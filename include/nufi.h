@@ -158,6 +158,10 @@ int nufi_check_status(nufi_handle *h);
 int nufi_mg_setup(nufi_handle *h, int world, int rank, int emulate, void *ipc_handle_out);
 int nufi_mg_connect(nufi_handle *h, const void *ipc_handles);
 int nufi_mg_handle_size(void);
+/* Leave multi-rank mode (frees the exchange buffers, closes the peers' IPC mappings); the
+ * handle then runs single-rank kernels again (e.g. after the ranks agreed to fall back to
+ * the per-step NCCL loop). */
+int nufi_mg_teardown(nufi_handle *h);
 
 /* Multi-rank d = 2, 3 step with the exchange FUSED into the block reduce (no NCCL):
  * after nufi_mg_setup / nufi_mg_connect on a d >= 2 handle, one call enqueues step n
@@ -192,6 +196,11 @@ int nufi_field_update(nufi_handle *h, const double *rho, double *W_out, double *
 int nufi_solve_poisson(nufi_handle *h, const double *rho, double *phi_out, double *spec_re, double *spec_im,
                        double *W_out);
 int nufi_fit_spline(nufi_handle *h, const double *phi, double *coeffs_out);
+/* transform_values / forward_transform (poisson.py:72-83): spectrum = fftn(values) / N^d
+ * (numpy FFT layout, real and imaginary parts, Nx^d each).  inverse_transform
+ * (poisson.py:85-87): values = Re ifftn(spectrum * N^d). */
+int nufi_transform_values(nufi_handle *h, const double *values, double *spec_re, double *spec_im);
+int nufi_inverse_transform(nufi_handle *h, const double *spec_re, const double *spec_im, double *values_out);
 
 /* One full step n (requires len == n): nufi_rho + nufi_field_update, all on
  * the device.  Outputs optional. */
@@ -221,6 +230,11 @@ int nufi_trace(nufi_handle *h, int64_t n, double *X, double *V, int64_t M, int h
  * run entry points (nufi_rho*, nufi_step*, nufi_run, nufi_moments) return
  * NUFI_ERR_USAGE. */
 int nufi_set_uniform_field(nufi_handle *h, int64_t step, const double *E0);
+/* FlowContext.install_field(step, SplineField) (flow.py:44-47): the spline with coefficient
+ * slab `coeffs` (Nx^d, row-major; host or device, copied) overrides stored field `step` for
+ * the point-level trace, evaluated like SplineField.eval_E_many (kernels.py:102-123);
+ * NULL removes it.  Same rules as nufi_set_uniform_field. */
+int nufi_set_spline_field(nufi_handle *h, int64_t step, const double *coeffs);
 int nufi_clear_fields(nufi_handle *h);
 
 /* Observable sweep at step n (density.quadrature_sweep_many, density.py:94-120,
@@ -240,6 +254,11 @@ int nufi_moments(nufi_handle *h, int64_t n, double *out, int64_t *evals);
  * the spline gradient, each optional; host or device buffers.  The numpy twin's
  * operation order, no FMA: bit-identical to the reference. */
 int nufi_eval_field(nufi_handle *h, int64_t slot, const double *X, int64_t M, double *phi_out, double *E_out);
+
+/* kernels.bspline_weights / bspline_dweights (kernels.py:62-81): the cubic B-spline stencil
+ * weights of M cell fractions t, w_out / dw_out (4, M) row-major (either may be NULL); numpy's
+ * operation order, no FMA (bit-identical). */
+int nufi_bspline_weights(nufi_handle *h, const double *t, int64_t M, double *w_out, double *dw_out);
 
 /* f0 at caller points (eval_f0, initial.py:165-180): F[M]. */
 int nufi_eval_f0(nufi_handle *h, const double *X, const double *V, int64_t M, double *F);

@@ -15,8 +15,10 @@ from .errors import ConfigError, FitError, NumericalConsistencyError, UsageError
 from .flow import (TRACE_FAST, TRACE_PARITY, FlowContext, eval_f, eval_f0, eval_f_batch, psi, psi_batch,
                    psi_tilde, psi_tilde_batch, trace_backward)
 from .grids import GridSpec, PhasePoint, v_mid, v_mid_matrix, x_node, x_node_matrix
-from .initial import BENCHMARK_DEFAULTS, InitialCondition, VelocityProfile, make_benchmark, weak_landau_3d
-from .poisson import SpectralField, electric_energy, solve_poisson, wavenumber_squared
+from .initial import (BENCHMARK_DEFAULTS, InitialCondition, VelocityProfile, background_density, make_benchmark,
+                      weak_landau_3d)
+from .poisson import (SpectralField, electric_energy, forward_transform, inverse_transform, solve_poisson,
+                      transform_values, wavenumber_squared)
 from .spline import PotentialHistory, SplineField, UniformField, fit_spline
 
 __version__ = "0.1.0"

@@ -95,6 +95,7 @@ _SIGS = {
     "nufi_mg_setup": [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P],
     "nufi_mg_connect": [_P, _P],
     "nufi_mg_handle_size": [],
+    "nufi_mg_teardown": [_P],
     "nufi_mg_step_async": [_P, _I64, _P, _P, _P, _P],
     "nufi_partials_len": [_P],
     "nufi_field_update": [_P, _P, _P, _P, _P],
@@ -102,11 +103,15 @@ _SIGS = {
     "nufi_run": [_P, _I64, _P, _P, _P, _P, _I64P],
     "nufi_trace": [_P, _I64, _P, _P, _I64, ctypes.c_int, ctypes.c_int, _I64P],
     "nufi_eval_f0": [_P, _P, _P, _I64, _P],
+    "nufi_bspline_weights": [_P, _P, _I64, _P, _P],
     "nufi_eval_field": [_P, _I64, _P, _I64, _P, _P],
     "nufi_set_uniform_field": [_P, _I64, _P],
+    "nufi_set_spline_field": [_P, _I64, _P],
     "nufi_clear_fields": [_P],
     "nufi_solve_poisson": [_P, _P, _P, _P, _P, _P],
     "nufi_fit_spline": [_P, _P, _P],
+    "nufi_transform_values": [_P, _P, _P, _P],
+    "nufi_inverse_transform": [_P, _P, _P, _P],
     "nufi_moments": [_P, _I64, _P, _I64P],
     "nufi_profiling": [_P, ctypes.c_int],
     "nufi_profiling_read": [_P, _P],

@@ -14,6 +14,7 @@
 #include <utility>
 #include <string>
 #include <algorithm>
+#include <map>
 #include <vector>
 
 #include "field_common.cuh"
@@ -32,9 +33,10 @@ cudaError_t launch_reduce_blocks(const double *partial, const double *fminmax, d
 cudaError_t launch_trace_points_ring(int d, bool pow2, const double *ev_hist, int ev_slab_elems, int N, double L,
                                      int n, double tau, double K, double *X, double *V, int64_t M, int half_kick,
                                      cudaStream_t st);
-cudaError_t launch_trace_points_generic(int d, const double *hist, int nodes, const double *ovr, int N, double L,
-                                        int n, double tau, double *X, double *V, int64_t M, int half_kick,
-                                        cudaStream_t st);
+cudaError_t launch_bspline_weights(const double *t, int64_t M, double *w, double *dw, cudaStream_t st);
+cudaError_t launch_trace_points_generic(int d, const double *hist, int nodes, const double *ovr,
+                                        const double *ovr_slabs, int N, double L, int n, double tau, double *X,
+                                        double *V, int64_t M, int half_kick, cudaStream_t st);
 cudaError_t launch_trace_points(int d, int mode, bool pow2, const double *hist, const double *ev_hist,
                                 int ev_slab_elems, int N, int nodes, double L, int n, double tau, double K, double *X,
                                 double *V, int64_t M, int half_kick, cudaStream_t st);
@@ -88,7 +90,7 @@ static int fail(int code, const std::string &msg) {
 // (including the early returns of CU).
 struct AsyncTemps {
     cudaStream_t st;
-    void *p[4] = {nullptr, nullptr, nullptr, nullptr};
+    void *p[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     int n = 0;
     explicit AsyncTemps(cudaStream_t s) : st(s) {}
     template <class T>
@@ -155,7 +157,8 @@ struct nufi_handle {
     int *mg_error = nullptr;
     // installed non-spline fields (FlowContext.install_field, flow.py:44-47): per step
     // [flag, E0_x, E0_y, E0_z]; honoured by the point-level trace (the reference's generic path)
-    std::vector<double> ovr;
+    std::vector<double> ovr;                        // per slot: kind (0 stored, 1 uniform, 2 spline) + 3 values
+    std::map<int64_t, std::vector<double>> ovr_spline;  // installed SplineField slabs by slot
     int64_t n_ovr = 0;
 
     int64_t len = 0;  // host mirror of the history length
@@ -332,10 +335,13 @@ static void choose_tiling(nufi_handle *h) {
             // ring (2 x 16 slabs) beats two 8-warp CTAs with 2 x 8 each (sl1 218.7 -> 203 ms)
             int sms = 148;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
-            const int64_t rows = per_block * (h->b_hi - h->b_lo), nt = (h->nodes + 31) / 32;
+            // rows of the FULL grid, not this rank's share: the tile height fixes how a block's
+            // rows are grouped when summed, so every rank count must pick the same one
+            const int64_t rows = per_block * h->B, nt = (h->nodes + 31) / 32;
             if ((rows / 16) * nt >= 2 * (int64_t)sms) warps = 16;
+            // the 16-warp (WIDE) run kernel exists for N = 256 only
+            if (const char *e = getenv("NUFI_D1_WARPS")) warps = atoi(e) >= 16 ? 16 : 8;
         }
-        if (const char *e = getenv("NUFI_D1_WARPS")) warps = atoi(e) >= 16 ? 16 : 8;
     } else if (h->d == 2) {
         warps = 8, ppt = 2, passes = 1;  // 2 interleaved points per thread, 2 CTAs / SM
     } else {
@@ -352,8 +358,9 @@ static void choose_tiling(nufi_handle *h) {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
         const int64_t nt = (h->nodes + 31) / 32;
-        // the rows THIS handle traces (a rank of a sharded run traces b_hi - b_lo blocks)
-        const int64_t rows = per_block * (h->b_hi - h->b_lo);
+        // rows of the full grid (see above): a sharded rank tiles exactly like one GPU, so its
+        // block sums -- and the history -- are bit-identical for every rank count
+        const int64_t rows = per_block * h->B;
         while (warps > 1 && (rows / (warps / 2)) * nt <= sms && per_block % (warps / 2) == 0) warps >>= 1;
     }
     while (ppt > 1 && (per_block % (warps * ppt) != 0)) ppt >>= 1;
@@ -582,6 +589,37 @@ int nufi_create(const nufi_config *cfg, int device, void *stream, nufi_handle **
     return NUFI_OK;
 }
 
+// Frees every multi-rank resource and returns the handle to single-rank mode.
+static void mg_release(nufi_handle *h) {
+    cudaStreamSynchronize(h->stream);
+    for (int q = 0; q < NUFI_MG_MAX; ++q) {
+        if (h->mg_opened[q]) cudaIpcCloseMemHandle(h->mg_peer[q]);
+        else if (h->mg_peer[q] && h->mg_peer[q] != h->mg_own) cudaFree(h->mg_peer[q]);
+        if (q > 0 && h->mg_part[q]) cudaFree(h->mg_part[q]);
+        if (q > 0 && h->mg_fmm[q]) cudaFree(h->mg_fmm[q]);
+        if (h->mg_bar[q] && h->mg_bar[q] != h->barrier) cudaFree(h->mg_bar[q]);
+        h->mg_opened[q] = false;
+        h->mg_peer[q] = nullptr;
+        if (q > 0) h->mg_part[q] = nullptr, h->mg_fmm[q] = nullptr;
+        h->mg_bar[q] = nullptr;
+    }
+    if (h->mg_own) cudaFree(h->mg_own);
+    if (h->mg_error) cudaFree(h->mg_error);
+    h->mg_own = nullptr;
+    h->mg_error = nullptr;
+    h->mg_world = 1;
+    h->mg_rank = 0;
+    h->mg_emulated = 0;
+    h->mg_steps = 0;
+}
+
+int nufi_mg_teardown(nufi_handle *h) {
+    CHECK_HANDLE(h);
+    mg_release(h);
+    CU(cudaGetLastError());
+    return NUFI_OK;
+}
+
 int nufi_destroy(nufi_handle *h) {
     if (!h) return NUFI_OK;
     cudaSetDevice(h->device);
@@ -592,15 +630,7 @@ int nufi_destroy(nufi_handle *h) {
                     (void *)h->ticket, (void *)h->barrier, (void *)h->mom_part, (void *)h->d_mom,
                     (void *)h->large_scratch, (void *)h->halo})
         if (p) cudaFreeAsync(p, h->stream);
-    for (int q = 0; q < NUFI_MG_MAX; ++q) {
-        if (h->mg_opened[q]) cudaIpcCloseMemHandle(h->mg_peer[q]);
-        else if (h->mg_peer[q] && h->mg_peer[q] != h->mg_own) cudaFree(h->mg_peer[q]);
-        if (q > 0 && h->mg_part[q]) cudaFree(h->mg_part[q]);
-        if (q > 0 && h->mg_fmm[q]) cudaFree(h->mg_fmm[q]);
-        if (h->mg_bar[q] && h->mg_bar[q] != h->barrier) cudaFree(h->mg_bar[q]);
-    }
-    if (h->mg_own) cudaFree(h->mg_own);
-    if (h->mg_error) cudaFree(h->mg_error);
+    mg_release(h);
     cudaStreamSynchronize(h->stream);  // frees complete -> the pool can hand the memory to the next handle
     pinned_put(h->run_host, h->run_elems);
     if (h->own_stream) cudaStreamDestroy(h->stream);
@@ -890,6 +920,7 @@ int nufi_set_uniform_field(nufi_handle *h, int64_t step, const double *E0) {
     if (step < 0) return fail(NUFI_ERR_USAGE, "step index must be >= 0");
     if ((size_t)(4 * (step + 1)) > h->ovr.size()) h->ovr.resize(4 * (size_t)(step + 1), 0.0);
     const bool was = h->ovr[4 * step] != 0.0;
+    h->ovr_spline.erase(step);
     if (E0) {
         h->ovr[4 * step] = 1.0;
         for (int a = 0; a < 3; ++a) h->ovr[4 * step + 1 + a] = a < h->d ? E0[a] : 0.0;
@@ -900,9 +931,32 @@ int nufi_set_uniform_field(nufi_handle *h, int64_t step, const double *E0) {
     return NUFI_OK;
 }
 
+int nufi_set_spline_field(nufi_handle *h, int64_t step, const double *coeffs) {
+    CHECK_HANDLE(h);
+    if (step < 0) return fail(NUFI_ERR_USAGE, "step index must be >= 0");
+    if ((size_t)(4 * (step + 1)) > h->ovr.size()) h->ovr.resize(4 * (size_t)(step + 1), 0.0);
+    const bool was = h->ovr[4 * step] != 0.0;
+    for (int a = 0; a < 4; ++a) h->ovr[4 * step + a] = 0.0;
+    h->ovr_spline.erase(step);
+    if (coeffs) {
+        std::vector<double> c((size_t)h->nodes);
+        if (is_device_ptr(coeffs)) {
+            CU(cudaMemcpyAsync(c.data(), coeffs, c.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+            CU(cudaStreamSynchronize(h->stream));
+        } else {
+            std::copy(coeffs, coeffs + c.size(), c.begin());
+        }
+        h->ovr_spline[step] = std::move(c);
+        h->ovr[4 * step] = 2.0;
+    }
+    h->n_ovr += (coeffs ? 1 : 0) - (was ? 1 : 0);
+    return NUFI_OK;
+}
+
 int nufi_clear_fields(nufi_handle *h) {
     CHECK_HANDLE(h);
     h->ovr.clear();
+    h->ovr_spline.clear();
     h->n_ovr = 0;
     return NUFI_OK;
 }
@@ -1440,10 +1494,23 @@ int nufi_trace(nufi_handle *h, int64_t n, double *X, double *V, int64_t M, int h
         // the reference's generic path (flow.py:65-82): every slot through its field object
         std::vector<double> tab(4 * (size_t)(n + 1), 0.0);
         std::copy(h->ovr.begin(), h->ovr.begin() + std::min(h->ovr.size(), tab.size()), tab.begin());
+        // installed SplineField slabs of slots 0..n, packed in slot order
+        std::vector<double> slabs;
+        for (const auto &kv : h->ovr_spline) {
+            if (kv.first > n) break;
+            tab[4 * (size_t)kv.first + 1] = (double)(slabs.size() / h->nodes);
+            slabs.insert(slabs.end(), kv.second.begin(), kv.second.end());
+        }
+        double *dslabs = nullptr;
         CU(tmp.alloc(&dovr, tab.size() * sizeof(double)));
         CU(cudaMemcpyAsync(dovr, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, h->stream));
-        CU(launch_trace_points_generic(h->d, h->hist, h->nodes, dovr, h->N, h->cfg.L, (int)n, h->cfg.tau, dX, dV, M,
-                                       half_kick ? 1 : 0, h->stream));
+        if (!slabs.empty()) {
+            CU(tmp.alloc(&dslabs, slabs.size() * sizeof(double)));
+            CU(cudaMemcpyAsync(dslabs, slabs.data(), slabs.size() * sizeof(double), cudaMemcpyHostToDevice,
+                               h->stream));
+        }
+        CU(launch_trace_points_generic(h->d, h->hist, h->nodes, dovr, dslabs, h->N, h->cfg.L, (int)n, h->cfg.tau, dX,
+                                       dV, M, half_kick ? 1 : 0, h->stream));
     } else {
         cudaError_t e = cudaErrorNotSupported;
         // d >= 2: slabs staged in a shared-memory ring (NUFI_TP_NORING=1: the in-place kernel, for tests)
@@ -1548,7 +1615,8 @@ int nufi_eval_field(nufi_handle *h, int64_t slot, const double *X, int64_t M, do
 static int poisson_fit(nufi_handle *h, int mode, const double *in, double *out, double *spec_re, double *spec_im,
                        double *W_out) {
     CHECK_HANDLE(h);
-    if (!in || !out) return fail(NUFI_ERR_USAGE, "null argument");
+    if (!in || (!out && mode != 2) || (mode >= 2 && (!spec_im || (mode == 2 && !spec_re))))
+        return fail(NUFI_ERR_USAGE, "null argument");
     const size_t bytes = (size_t)h->nodes * sizeof(double);
     // device staging: in, out, spec re / im, W (one allocation)
     double *buf = nullptr;
@@ -1557,14 +1625,17 @@ static int poisson_fit(nufi_handle *h, int mode, const double *in, double *out, 
     double *din = buf, *dout = buf + h->nodes, *dre = buf + 2 * h->nodes, *dim = buf + 3 * h->nodes,
            *dW = buf + 4 * h->nodes;
     CU(cudaMemcpyAsync(din, in, bytes, cudaMemcpyDefault, h->stream));
+    if (mode == 3) CU(cudaMemcpyAsync(dim, spec_im, bytes, cudaMemcpyDefault, h->stream));  // input
     CU(cudaMemsetAsync(h->d_status, 0, sizeof(int), h->stream));
     FieldParams f = field_params(h);
     CU(launch_poisson_fit(f, mode, din, dout, dre, dim, dW, h->d_status, h->stream));
     int st = 0;
     CU(cudaMemcpyAsync(&st, h->d_status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-    CU(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDefault, h->stream));
-    if (spec_re) CU(cudaMemcpyAsync(spec_re, dre, bytes, cudaMemcpyDefault, h->stream));
-    if (spec_im) CU(cudaMemcpyAsync(spec_im, dim, bytes, cudaMemcpyDefault, h->stream));
+    if (out) CU(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDefault, h->stream));
+    if (mode != 3) {
+        if (spec_re) CU(cudaMemcpyAsync(spec_re, dre, bytes, cudaMemcpyDefault, h->stream));
+        if (spec_im) CU(cudaMemcpyAsync(spec_im, dim, bytes, cudaMemcpyDefault, h->stream));
+    }
     if (W_out) CU(cudaMemcpyAsync(W_out, dW, sizeof(double), cudaMemcpyDefault, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     if (st == NUFI_ERR_NUMERICAL) {
@@ -1582,6 +1653,38 @@ int nufi_solve_poisson(nufi_handle *h, const double *rho, double *phi_out, doubl
 
 int nufi_fit_spline(nufi_handle *h, const double *phi, double *coeffs_out) {
     return poisson_fit(h, 1, phi, coeffs_out, nullptr, nullptr, nullptr);
+}
+
+int nufi_transform_values(nufi_handle *h, const double *values, double *spec_re, double *spec_im) {
+    return poisson_fit(h, 2, values, nullptr, spec_re, spec_im, nullptr);
+}
+
+int nufi_inverse_transform(nufi_handle *h, const double *spec_re, const double *spec_im, double *values_out) {
+    return poisson_fit(h, 3, spec_re, values_out, nullptr, const_cast<double *>(spec_im), nullptr);
+}
+
+int nufi_bspline_weights(nufi_handle *h, const double *t, int64_t M, double *w_out, double *dw_out) {
+    CHECK_HANDLE(h);
+    if (M == 0) return NUFI_OK;
+    if (!t || (!w_out && !dw_out)) return fail(NUFI_ERR_USAGE, "null argument");
+    const size_t bytes = (size_t)M * sizeof(double);
+    AsyncTemps tmp(h->stream);
+    const double *dt = t;
+    double *dw = w_out, *ddw = dw_out;
+    if (!is_device_ptr(t)) {
+        double *p = nullptr;
+        CU(tmp.alloc(&p, bytes));
+        CU(cudaMemcpyAsync(p, t, bytes, cudaMemcpyHostToDevice, h->stream));
+        dt = p;
+    }
+    const bool hw = w_out && !is_device_ptr(w_out), hdw = dw_out && !is_device_ptr(dw_out);
+    if (hw) CU(tmp.alloc(&dw, 4 * bytes));
+    if (hdw) CU(tmp.alloc(&ddw, 4 * bytes));
+    CU(launch_bspline_weights(dt, M, dw, ddw, h->stream));
+    if (hw) CU(cudaMemcpyAsync(w_out, dw, 4 * bytes, cudaMemcpyDeviceToHost, h->stream));
+    if (hdw) CU(cudaMemcpyAsync(dw_out, ddw, 4 * bytes, cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    return NUFI_OK;
 }
 
 int nufi_eval_f0(nufi_handle *h, const double *X, const double *V, int64_t M, double *F) {

@@ -47,6 +47,9 @@ __global__ void __launch_bounds__(1024) field_update_kernel(const FieldParams p)
 //           spec = fftn(rho) / N^d / k^2 with the zero and Nyquist modes dropped,
 //           phi = Re ifftn(spec * N^d); W = L^d / 2 sum k^2 |spec|^2 (poisson.py:115-120)
 //   mode 1  fit_spline (spline.py:71-86): coeffs = Re ifftn(fftn(phi) / prod sym)
+//   mode 2  transform_values (poisson.py:72-78): spec = fftn(in) / N^d -> spec_re, spec_im
+//   mode 3  inverse_transform (poisson.py:85-87): out = Re ifftn(spec * N^d), spectrum
+//           read from in (real part) and spec_im (imaginary part, an INPUT here)
 // in: Nx^d reals; out: Nx^d reals; spec_re / spec_im / W optional (mode 0).
 __global__ void __launch_bounds__(1024) poisson_fit_kernel(FieldParams p, int mode, const double *in, double *out,
                                                            double *spec_re, double *spec_im, double *W_out,
@@ -64,7 +67,7 @@ __global__ void __launch_bounds__(1024) poisson_fit_kernel(FieldParams p, int mo
     for (int i = threadIdx.x; i < nodes; i += T) {
         const double v = in[i];
         ar[i] = v;
-        ai[i] = 0.0;
+        ai[i] = mode == 3 ? spec_im[i] : 0.0;
         s += v;
         mx = fmax(mx, fabs(v));
     }
@@ -79,15 +82,22 @@ __global__ void __launch_bounds__(1024) poisson_fit_kernel(FieldParams p, int mo
     __syncthreads();
     int G = 1;
     while (G < 32 && 2 * G <= N && (long long)nodes * 2 * G <= 256) G *= 2;
-    for (int axis = d - 1; axis >= 0; --axis) {
+    for (int axis = d - 1; axis >= 0 && mode != 3; --axis) {
         int st = 1;
         for (int a = axis + 1; a < d; ++a) st *= N;
         dft_pass(ar, ai, br, bi, twc, tws, N, nodes, st, -1.0, G, pow2);
         double *tr = ar, *ti = ai;
         ar = br, ai = bi, br = tr, bi = ti;
     }
+    if (mode == 2) {  // poisson.py:77: fftn(values) / grid.n_nodes
+        for (int e = threadIdx.x; e < nodes; e += T) {
+            spec_re[e] = ar[e] / (double)nodes;
+            spec_im[e] = ai[e] / (double)nodes;
+        }
+        return;
+    }
     double wsum = 0.0;
-    for (int e = threadIdx.x; e < nodes; e += T) {
+    for (int e = threadIdx.x; e < nodes && mode != 3; e += T) {
         const double sym = p.fac[nodes + e];
         double f;
         if (mode == 0) {

@@ -336,6 +336,26 @@ __device__ __forceinline__ void field_numpy(const double *__restrict__ c, int N,
         for (int g = 0; g < D; ++g) E_out[g] = M_(E[g], inv_h);
 }
 
+// kernels.bspline_weights / bspline_dweights (kernels.py:62-81) at M fractions t:
+// w[m * M + p], dw[m * M + p] (the reference's (4,) + t.shape layout), numpy's operations.
+__global__ void bspline_weights_kernel(const double *__restrict__ t, int64_t M, double *w, double *dw) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= M) return;
+    double a[4], b[4];
+    fill_weights_exact(t[p], a, b);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        if (w) w[m * M + p] = a[m];
+        if (dw) dw[m * M + p] = b[m];
+    }
+}
+
+cudaError_t launch_bspline_weights(const double *t, int64_t M, double *w, double *dw, cudaStream_t st) {
+    const int threads = 256;
+    bspline_weights_kernel<<<(unsigned)((M + threads - 1) / threads), threads, 0, st>>>(t, M, w, dw);
+    return cudaGetLastError();
+}
+
 template <int D>
 __global__ void eval_field_kernel(const double *__restrict__ c, int N, double L, const double *__restrict__ X,
                                   int64_t M, double *__restrict__ phi_out, double *__restrict__ E_out) {
@@ -354,8 +374,8 @@ __global__ void eval_field_kernel(const double *__restrict__ c, int N, double L,
 // ovr[4k] != 0, E0 = ovr[4k+1 ..]) or the stored spline's eval_E_many.
 template <int D>
 __global__ void trace_points_generic(const double *__restrict__ hist, int nodes, const double *__restrict__ ovr,
-                                     int N, double L, int n, double tau, double *X, double *V, int64_t M,
-                                     int half_kick) {
+                                     const double *__restrict__ ovr_slabs, int N, double L, int n, double tau,
+                                     double *X, double *V, int64_t M, int half_kick) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= M) return;
     const double inv_h = (double)N / L;
@@ -366,10 +386,15 @@ __global__ void trace_points_generic(const double *__restrict__ hist, int nodes,
         x[a] = X[p * D + a];
         v[a] = V[p * D + a];
     }
+    // slot k: ovr[4k] = 0 the stored spline, 1 a UniformField (E0 = ovr[4k+1..]), 2 an
+    // installed SplineField (its slab is ovr_slabs row ovr[4k+1])
     auto field = [&](int k) {
-        if (ovr[4 * (size_t)k] != 0.0) {
+        const double kind = ovr[4 * (size_t)k];
+        if (kind == 1.0) {
 #pragma unroll
             for (int a = 0; a < D; ++a) E[a] = ovr[4 * (size_t)k + 1 + a];
+        } else if (kind == 2.0) {
+            field_numpy<D>(ovr_slabs + (size_t)ovr[4 * (size_t)k + 1] * nodes, N, L, inv_h, x, nullptr, E);
         } else {
             field_numpy<D>(hist + (size_t)k * nodes, N, L, inv_h, x, nullptr, E);
         }
@@ -452,14 +477,19 @@ cudaError_t launch_trace_points(int d, int mode, bool pow2, const double *hist, 
     return cudaGetLastError();
 }
 
-cudaError_t launch_trace_points_generic(int d, const double *hist, int nodes, const double *ovr, int N, double L,
-                                        int n, double tau, double *X, double *V, int64_t M, int half_kick,
-                                        cudaStream_t st) {
+cudaError_t launch_trace_points_generic(int d, const double *hist, int nodes, const double *ovr,
+                                        const double *ovr_slabs, int N, double L, int n, double tau, double *X,
+                                        double *V, int64_t M, int half_kick, cudaStream_t st) {
     const int threads = 128;
     const int ctas = (int)((M + threads - 1) / threads);
-    if (d == 1) trace_points_generic<1><<<ctas, threads, 0, st>>>(hist, nodes, ovr, N, L, n, tau, X, V, M, half_kick);
-    if (d == 2) trace_points_generic<2><<<ctas, threads, 0, st>>>(hist, nodes, ovr, N, L, n, tau, X, V, M, half_kick);
-    if (d == 3) trace_points_generic<3><<<ctas, threads, 0, st>>>(hist, nodes, ovr, N, L, n, tau, X, V, M, half_kick);
+#define NUFI_TPG(DD)                                                                                        \
+    if (d == DD)                                                                                            \
+        trace_points_generic<DD><<<ctas, threads, 0, st>>>(hist, nodes, ovr, ovr_slabs, N, L, n, tau, X, V, M, \
+                                                           half_kick);
+    NUFI_TPG(1)
+    NUFI_TPG(2)
+    NUFI_TPG(3)
+#undef NUFI_TPG
     return cudaGetLastError();
 }
 

@@ -43,9 +43,14 @@ __global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams 
     const int slab_elems = p.ev_slab_elems;
 
     double *ring = reinterpret_cast<double *>(smem_raw);
-    uint64_t *full = reinterpret_cast<uint64_t *>(ring + (GL ? 0 : (size_t)stages * sps * slab_elems));
+    // the mbarriers sit after max(ring, red) -- the CTA reduction below may need more
+    // room than the ring (MOM sweeps on small grids) and must never overwrite them
+    // (same layout as trace_rho_smem_bytes)
+    const size_t ring_elems = GL ? 0 : (size_t)stages * sps * slab_elems;
+    const size_t red_elems = (size_t)(mom_sums(3) + 2) * blockDim.x;
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + (ring_elems > red_elems ? ring_elems : red_elems));
     uint64_t *empty = full + stages;
-    double *red = ring;  // 3 * blockDim.x, aliases the ring once every stage is consumed
+    double *red = ring;  // aliases the ring once every stage is consumed
 
     const int tile = blockIdx.x % p.node_tiles;
     const int vt = p.vt_lo + blockIdx.x / p.node_tiles;

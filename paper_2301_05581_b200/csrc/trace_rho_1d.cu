@@ -199,6 +199,7 @@ int trace_rho_1d_sps(int N, bool wide) {
     if (N == 32) return 16;
     if (N == 128) return 8;
     if (N == 256) {
+        if (wide) return 16;  // the WIDE run kernel is instantiated for 2 x 16 slabs only
         if (const char *e = getenv("NUFI_D1_SPS")) {
             const int v = atoi(e);
             if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) return v;

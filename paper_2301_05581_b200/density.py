@@ -112,7 +112,7 @@ def _batches(ctx: FlowContext, n: int, chunk: int):
         Xb = np.repeat(Xn[start:stop], n_cells, axis=0)
         Vb = np.tile(Vm, (stop - start, 1))
         Xt, Vt = psi_batch(ctx, n, Xb, Vb)  # GPU trace (nufi_trace)
-        F = eval_f0(ctx, Xt, Vt)  # GPU f0 (nufi_eval_f0)
+        F = eval_f0(ctx.ic, Xt, Vt)  # GPU f0 (nufi_eval_f0)
         yield slice(start, stop), Xb, Vb, F
 
 

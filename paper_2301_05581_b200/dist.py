@@ -1,4 +1,4 @@
-"""Multi-GPU NuFI: quadrature points sharded by velocity blocks, one allreduce per step.
+"""Multi-GPU NuFI: quadrature points sharded by velocity blocks, one exchange per step.
 
 One process per GPU (torch.distributed, NCCL over NVLink for the plumbing).
 The Nv^d velocity rows are cut into B fixed blocks (default 8, independent of
@@ -14,13 +14,17 @@ spline / append (nufi_step_finish) and therefore holds a bit-identical full
 history.  Because the combine order over blocks does not depend on G, the
 result is bit-identical for G = 1, 2, 4, 8.
 
-The compute callable is injectable so the exchange logic can be tested on CPU
-ranks (gloo) with a reference implementation of the block sums.
+The exchange is either the per-step NCCL allreduce of that table (default) or,
+with NUFI_MG=1, fused into our own kernels over CUDA-IPC peer memory (the d = 1
+persistent run kernel / the d >= 2 block reduce store the block sums straight into
+every peer's table); the fused path is opt-in until it has run on more than one
+physical GPU.  `exchange` names the path a run took.
 """
 
 from __future__ import annotations
 
 import ctypes
+import functools
 import os
 from dataclasses import dataclass
 
@@ -36,6 +40,24 @@ def block_range(B: int, rank: int, world: int) -> tuple[int, int]:
     lo = (B * rank) // world
     hi = (B * (rank + 1)) // world
     return lo, hi
+
+
+def _on_stream(fn):
+    """Run a DistributedSimulation method with its stream current, so torch collectives and
+    tensor ops are ordered with the library's kernels."""
+
+    @functools.wraps(fn)
+    def wrapper(self, *args, **kwargs):
+        cur = self.torch.cuda.current_stream(self.stream.device)
+        if cur != self.stream:
+            self.stream.wait_stream(cur)
+        with self.torch.cuda.stream(self.stream):
+            out = fn(self, *args, **kwargs)
+        if cur != self.stream:
+            cur.wait_stream(self.stream)
+        return out
+
+    return wrapper
 
 
 @dataclass
@@ -86,7 +108,11 @@ class DistributedSimulation:
         self.B = B
         lo, hi = block_range(B, self.rank, self.world)
         device = torch.cuda.current_device()
-        self.stream = torch.cuda.current_stream(device)
+        # The library and the collectives must share ONE stream.  The legacy default stream
+        # (cuda_stream == 0) cannot be handed to the library (NULL means "private stream"),
+        # so a run started on it gets a dedicated stream, made current around every step.
+        cur = torch.cuda.current_stream(device)
+        self.stream = cur if cur.cuda_stream != 0 else torch.cuda.Stream(device)
         from .flow import FlowContext
         from .spline import PotentialHistory
 
@@ -96,35 +122,67 @@ class DistributedSimulation:
                                         block_range=(lo, hi), stream=self.stream.cuda_stream)
         self.ctx = FlowContext(history=self.history, ic=ic, tau=tau, grid=grid)
         n = int(self.history.handle.lib.nufi_partials_len(self.history.handle.h))
-        self.partials = torch.zeros(n, dtype=torch.float64, device=f"cuda:{device}")
+        with torch.cuda.stream(self.stream):
+            self.partials = torch.zeros(n, dtype=torch.float64, device=f"cuda:{device}")
+        self.stream.wait_stream(cur)  # the caller's pending work (e.g. output allocation) first
         self.block_lo, self.block_hi = lo, hi
         self.fused = False
-        if self.world > 1 and B % self.world == 0 and os.environ.get("NUFI_MG", "1") != "0":
+        # The fused peer-memory exchange is opt-in (NUFI_MG=1) until it has run on more
+        # than one physical GPU; the default is the per-step NCCL allreduce loop.
+        if self.world > 1 and B % self.world == 0 and os.environ.get("NUFI_MG", "0") == "1":
             self._connect_fused(device)
 
+    @property
+    def exchange(self) -> str:
+        """The exchange the next run takes: "fused-ipc" or "nccl-allreduce" (single rank: "none")."""
+        if self.world == 1:
+            return "none"
+        return "fused-ipc" if self.fused else "nccl-allreduce"
+
+    @_on_stream
     def _connect_fused(self, device: int) -> None:
         """The exchange fused into our own kernels (nufi_mg_*): d = 1 the persistent run
         kernel, d = 2, 3 the block reduce (nufi_mg_step_async).  Every rank exports its
         exchange buffer (CUDA IPC), the handles are all-gathered over the process group,
-        every rank opens its peers'.  Falls back to the per-step NCCL loop (with a
-        warning) if peer memory is unavailable or the grid needs the multi-CTA tail."""
+        every rank opens its peers'.  The ranks decide TOGETHER: every rank reaches the
+        all_gather (with an ok byte in front of its handle, 0 if its setup failed) and the
+        final all_reduce(MIN) of the connect outcome, so either all ranks run fused or all
+        fall back to the per-step NCCL loop (with a warning) -- never a split decision
+        that would leave the ranks in mismatched collectives."""
         import warnings
 
+        t = self.torch
         h = self.history.handle
+        size = int(h.lib.nufi_mg_handle_size())
+        buf = ctypes.create_string_buffer(size)
+        ok = 1
+        why = None
         try:
-            size = int(h.lib.nufi_mg_handle_size())
-            buf = ctypes.create_string_buffer(size)
             h.call("nufi_mg_setup", self.world, self.rank, 0, buf)
-            mine = self.torch.tensor(list(buf.raw), dtype=self.torch.uint8, device=f"cuda:{device}")
-            allh = [self.torch.empty_like(mine) for _ in range(self.world)]
-            self.dist.all_gather(allh, mine, group=self.group)
-            blob = bytes(b for t in allh for b in t.cpu().tolist())
-            h.call("nufi_mg_connect", blob)
-            self.dist.barrier(group=self.group)  # every rank connected before any kernel runs
-            self.fused = True
         except Exception as exc:  # pragma: no cover - depends on the machine's peer access
-            warnings.warn(f"fused multi-rank kernel unavailable ({exc}); using the per-step NCCL loop")
-            self.fused = False
+            ok, why = 0, exc
+        # NCCL gathers device tensors; gloo (CPU-side test groups) gathers host tensors
+        where = f"cuda:{device}" if self.dist.get_backend(self.group) == "nccl" else "cpu"
+        mine = t.tensor([ok] + list(buf.raw), dtype=t.uint8, device=where)
+        allh = [t.empty_like(mine) for _ in range(self.world)]
+        self.dist.all_gather(allh, mine, group=self.group)
+        rows = [bytes(x.cpu().tolist()) for x in allh]
+        if all(r[0] == 1 for r in rows):
+            try:
+                h.call("nufi_mg_connect", b"".join(r[1:] for r in rows))
+            except Exception as exc:  # pragma: no cover
+                ok, why = 0, exc
+        else:
+            ok = 0
+            why = why or "a peer's peer-memory setup failed"
+        flag = t.tensor([ok], dtype=t.int32, device=where)
+        self.dist.all_reduce(flag, op=self.dist.ReduceOp.MIN, group=self.group)
+        self.fused = int(flag.item()) == 1
+        if not self.fused:
+            warnings.warn(f"fused multi-rank kernel unavailable ({why or 'on a peer'}); "
+                          "using the per-step NCCL loop")
+            if ok:
+                h.call("nufi_mg_teardown")
 
     def _run_exchange_steps(self, first: int, outputs: dict, ev) -> None:
         """d = 2, 3 fused loop: nufi_mg_step_async per step (trace own blocks -> block sums
@@ -157,6 +215,7 @@ class DistributedSimulation:
         per_step = g.n_nodes * g.n_cells * (self.block_hi - self.block_lo) // self.B
         ev.value += per_step * sum(range(first, self.n_steps + 1))
 
+    @_on_stream
     def step(self, outputs: dict | None = None, row: int = 0, sync: bool = True):
         """One step: trace own blocks -> allreduce -> redundant field update."""
         h = self.history.handle
@@ -182,6 +241,7 @@ class DistributedSimulation:
         self.ctx.field_evals += int(ev.value)
         return n
 
+    @_on_stream
     def run(self, outputs: dict | None = None):
         """The whole loop.  With device (CUDA tensor) outputs every step is enqueued
         without a host synchronisation (trace -> NCCL allreduce -> field update, all on
@@ -226,6 +286,7 @@ class DistributedSimulation:
 
             warnings.warn(f"fused multi-rank run failed ({err or 'on a peer'}); rerunning with the per-step NCCL loop")
             self.fused = False
+            self.history.handle.call("nufi_mg_teardown")
             self.history.truncate(first)
         host = outputs is None
         if host:

@@ -7,9 +7,10 @@ runs in libnufi_b200 (nufi_trace -> csrc/trace_points.cu); f0 is evaluated on
 the device (nufi_eval_f0).
 
 `install_field` (flow.py:44-47, the reference's test hook that overrides a stored
-field) takes UniformField objects (spline.py:55-68): while any is installed, the
-point-level trace follows the reference's generic path (flow.py:65-82) on the GPU
-(csrc/trace_points.cu trace_points_generic), for the constant-force closed-form tests.
+field) takes UniformField (spline.py:55-68) and SplineField objects: while any is
+installed, the point-level trace follows the reference's generic path (flow.py:65-82)
+on the GPU (csrc/trace_points.cu trace_points_generic), for the constant-force
+closed-form tests and field-substitution experiments.
 """
 
 from __future__ import annotations
@@ -21,7 +22,7 @@ import numpy as np
 from . import _lib
 from .errors import UsageError
 from .grids import GridSpec, PhasePoint
-from .initial import InitialCondition
+from .initial import InitialCondition, background_density, eval_f0  # noqa: F401  (flow.py:21 re-exports)
 from .spline import PotentialHistory
 
 TRACE_FAST = _lib.NUFI_TRACE_FAST
@@ -56,18 +57,27 @@ class FlowContext:
 
     def install_field(self, step: int, fld) -> None:
         """Override the stored field at one step (flow.py:44-47, testing hook).  Accepts a
-        UniformField (or None to remove the override); the override lives on the history
-        (its device handle), so every context over that history sees it."""
-        from .spline import UniformField
+        UniformField (spline.py:55-68) or a SplineField on this grid (spline.py:28-52; its
+        coefficient slab is uploaded and evaluated on the device like eval_E_many), or None
+        to remove the override.  The override lives on the history (its device handle), so
+        every context over that history sees it.  Other Python field objects cannot be
+        evaluated by the device trace and raise UsageError."""
+        from .spline import SplineField, UniformField
 
         if int(step) < 0:
             raise UsageError("step index must be >= 0")
         if fld is None:
             self.history.handle.call("nufi_set_uniform_field", int(step), None)
             return
+        if isinstance(fld, SplineField):
+            if fld.grid.d != self.grid.d or fld.grid.Nx != self.grid.Nx or fld.grid.L != self.grid.L:
+                raise UsageError("SplineField grid (d, Nx, L) does not match the context grid")
+            c = np.ascontiguousarray(fld.coeffs, dtype=np.float64).reshape(-1)
+            self.history.handle.call("nufi_set_spline_field", int(step), c.ctypes.data)
+            return
         if not isinstance(fld, UniformField):
-            raise UsageError("the GPU trace accepts UniformField overrides only (spline fields are stored "
-                             "with PotentialHistory.append)")
+            raise UsageError("the GPU trace accepts UniformField or SplineField overrides only, got "
+                             f"{type(fld).__name__}")
         if fld.d != self.grid.d:
             raise UsageError(f"UniformField has {fld.d} components, the grid has d = {self.grid.d}")
         E0 = np.ascontiguousarray(fld.E0, dtype=np.float64)
@@ -129,21 +139,10 @@ def psi_tilde(ctx: FlowContext, n: int, p: PhasePoint) -> PhasePoint:
     return PhasePoint(x=X[0], v=V[0])
 
 
-def eval_f0(ctx: FlowContext, X, V) -> np.ndarray:
-    """f0 at (M, d) points on the GPU (initial.py:165-180)."""
-    X = np.ascontiguousarray(X, dtype=np.float64)
-    V = np.ascontiguousarray(V, dtype=np.float64)
-    if X.shape != V.shape or X.ndim != 2 or X.shape[1] != ctx.grid.d:
-        raise UsageError(f"x and v must both have shape (M, {ctx.grid.d})")
-    F = np.empty(X.shape[0])
-    ctx.history.handle.call("nufi_eval_f0", X.ctypes.data, V.ctypes.data, int(X.shape[0]), F.ctypes.data)
-    return F
-
-
 def eval_f_batch(ctx: FlowContext, n: int, x, v) -> np.ndarray:
     """f(n tau, x, v) = f0(Psi(x, v)) (flow.py:134-137)."""
     X, V = psi_batch(ctx, n, x, v)
-    return eval_f0(ctx, X, V)
+    return eval_f0(ctx.ic, X, V)
 
 
 def eval_f(ctx: FlowContext, n: int, p: PhasePoint) -> float:

@@ -14,6 +14,8 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass, field
 
+import numpy as np
+
 from .errors import UsageError
 
 GAUSS_NORM = 1.0 / math.sqrt(2.0 * math.pi)  # initial.py:22
@@ -111,3 +113,59 @@ def weak_landau_3d(alpha: float = 0.01, k: float = 0.5, L: float = 4.0 * math.pi
     way SURVEY.md §8(d) maps it onto InitialCondition (initial.py:72-106)."""
     return InitialCondition(benchmark="weak_landau_3d", d=3, L=L, alpha=alpha, k=k,
                             profiles=(VelocityProfile(),) * 3)
+
+
+# ---------------------------------------------------------------------------
+# f0 and the background density on the device (the reference's module functions)
+# ---------------------------------------------------------------------------
+
+_f0_handles: dict = {}
+_rho_bar_cache: dict = {}
+
+
+def _f0_history(ic: InitialCondition):
+    """A 1-slab device handle carrying ic's f0 descriptor (cached per initial condition)."""
+    h = _f0_handles.get(ic)
+    if h is None:
+        from .grids import GridSpec
+        from .spline import PotentialHistory
+
+        g = GridSpec(d=ic.d, L=ic.L, Nx=4, Nv=2, vmax=1.0)  # only d and L matter for f0
+        h = PotentialHistory(g, 1.0, capacity=1)
+        h.bind(ic, rho_bar=ic.rho_bar)
+        _f0_handles[ic] = h
+    return h
+
+
+def eval_f0(ic: InitialCondition, x, v) -> np.ndarray:
+    """f0 at positions x and velocities v of shape (..., d) (initial.py:165-180), evaluated by
+    the device kernel (nufi_eval_f0) on the unwrapped x.  Returns shape (...)."""
+    x = np.asarray(x, dtype=np.float64)
+    v = np.asarray(v, dtype=np.float64)
+    if x.shape != v.shape or x.shape[-1:] != (ic.d,):
+        raise UsageError(f"x and v must both end in a length-{ic.d} axis")
+    X = np.ascontiguousarray(x.reshape(-1, ic.d))
+    V = np.ascontiguousarray(v.reshape(-1, ic.d))
+    F = np.empty(X.shape[0])
+    if F.size:
+        _f0_history(ic).handle.call("nufi_eval_f0", X.ctypes.data, V.ctypes.data, int(X.shape[0]), F.ctypes.data)
+    return F.reshape(x.shape[:-1])
+
+
+def f0_at(ic: InitialCondition, p) -> float:
+    """f0 at one PhasePoint (initial.py:183-184)."""
+    return float(eval_f0(ic, p.x, p.v))
+
+
+def background_density(ic: InitialCondition, grid) -> float:
+    """Midpoint-quadrature background density on the run's phase grid (initial.py:187-208),
+    computed by the device's rho_bar kernel (the reference's factorised x-sum x v-sum)."""
+    if grid.d != ic.d:
+        raise UsageError(f"grid dimension {grid.d} does not match benchmark dimension {ic.d}")
+    key = (ic, grid)
+    if key not in _rho_bar_cache:
+        from .spline import PotentialHistory
+
+        h = PotentialHistory(grid, 1.0, capacity=1)
+        _rho_bar_cache[key] = h.bind(ic)
+    return _rho_bar_cache[key]

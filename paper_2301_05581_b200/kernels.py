@@ -79,3 +79,54 @@ def trace_backward(coeffs, L: float, n: int, tau: float, X: np.ndarray, V: np.nd
     h.handle.call("nufi_trace", int(n), X.ctypes.data, V.ctypes.data, int(X.shape[0]), int(bool(half_kick)),
                   int(_BACKENDS[_backend]), _lib.ctypes.byref(evals))
     return int(evals.value)
+
+
+# ---------------------------------------------------------------------------
+# The reference's spline helpers (kernels.py:62-123), on the device
+# ---------------------------------------------------------------------------
+
+def _helper_history():
+    from .spline import _scratch_history
+
+    return _scratch_history(GridSpec(d=1, L=1.0, Nx=4, Nv=2, vmax=1.0))
+
+
+def _weights(t, which: str) -> np.ndarray:
+    t = np.ascontiguousarray(np.asarray(t, dtype=np.float64))
+    out = np.empty((4,) + t.shape)
+    if t.size:
+        w = out.ctypes.data if which == "w" else None
+        dw = out.ctypes.data if which == "dw" else None
+        _helper_history().handle.call("nufi_bspline_weights", t.ctypes.data, int(t.size), w, dw)
+    return out
+
+
+def bspline_weights(t) -> np.ndarray:
+    """Cubic B-spline values for the 4-node stencil, shape (4,) + t.shape (kernels.py:62-70);
+    bit-identical (numpy's operation order, no FMA; nufi_bspline_weights)."""
+    return _weights(t, "w")
+
+
+def bspline_dweights(t) -> np.ndarray:
+    """Stencil weights of d/dt, shape (4,) + t.shape (kernels.py:73-81)."""
+    return _weights(t, "dw")
+
+
+def _spline_field(coeffs, L: float, X):
+    from .spline import SplineField
+
+    c = np.asarray(coeffs, dtype=np.float64)
+    X = np.asarray(X)
+    if X.ndim != 2 or c.ndim != X.shape[1]:
+        raise UsageError("X must have shape (M, d) and coeffs shape (N,)*d")
+    return SplineField(grid=GridSpec(d=c.ndim, L=float(L), Nx=c.shape[0], Nv=2, vmax=1.0), coeffs=c)
+
+
+def eval_phi_many(coeffs, L: float, X) -> np.ndarray:
+    """Spline values at X (M, d) for a (N,)*d coefficient grid (kernels.py:84-99), on the device."""
+    return _spline_field(coeffs, L, X).eval_phi_many(X)
+
+
+def eval_E_many(coeffs, L: float, X) -> np.ndarray:
+    """Minus the spline gradient at X, shape (M, d) (kernels.py:102-123), on the device."""
+    return _spline_field(coeffs, L, X).eval_E_many(X)

@@ -40,6 +40,37 @@ def wavenumber_squared(grid: GridSpec) -> np.ndarray:
     return k2
 
 
+def transform_values(grid: GridSpec, values) -> SpectralField:
+    """Trigonometric interpolant coefficients fftn(values) / N^d of real nodal values
+    (poisson.py:72-78), by the device's separable DFT passes (nufi_transform_values)."""
+    values = np.asarray(values, dtype=np.float64)
+    if values.shape != grid.shape_x:
+        raise UsageError(f"values must have shape {grid.shape_x}, got {values.shape}")
+    vals = np.ascontiguousarray(values).reshape(-1)
+    re = np.empty(grid.n_nodes)
+    im = np.empty(grid.n_nodes)
+    _scratch_history(grid).handle.call("nufi_transform_values", vals.ctypes.data, re.ctypes.data, im.ctypes.data)
+    return SpectralField(grid=grid, coeffs=(re + 1j * im).reshape(grid.shape_x))
+
+
+def forward_transform(rho: DensityGrid) -> SpectralField:
+    """poisson.py:81-82."""
+    return transform_values(rho.grid, rho.values)
+
+
+def inverse_transform(spectrum: SpectralField) -> np.ndarray:
+    """Real nodal values Re ifftn(coeffs * N^d) of the interpolant (poisson.py:85-87), on the device."""
+    g = spectrum.grid
+    c = np.asarray(spectrum.coeffs)
+    if c.shape != g.shape_x:
+        raise UsageError(f"spectrum must have shape {g.shape_x}")
+    re = np.ascontiguousarray(c.real, dtype=np.float64).reshape(-1)
+    im = np.ascontiguousarray(c.imag if np.iscomplexobj(c) else np.zeros(c.shape), dtype=np.float64).reshape(-1)
+    out = np.empty(g.n_nodes)
+    _scratch_history(g).handle.call("nufi_inverse_transform", re.ctypes.data, im.ctypes.data, out.ctypes.data)
+    return out.reshape(g.shape_x)
+
+
 def solve_poisson(rho: DensityGrid) -> tuple[np.ndarray, SpectralField]:
     """-laplace(phi) = rho on the torus (poisson.py:90-112), on the GPU.  Raises
     NumericalConsistencyError when |mean rho| > 1e-8 max|rho|."""

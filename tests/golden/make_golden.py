@@ -45,7 +45,10 @@ CONFIGS = {
     "ts1": dict(d=1, Nx=64, Nv=512, vmax=10.0, tau=1 / 16, N=1600, bench="two_stream_1d", alpha=None, keep=51),
     "sl1": dict(d=1, Nx=256, Nv=2048, vmax=8.0, tau=1 / 16, N=800, bench="weak_landau_1d", alpha=0.5, keep=51),
     "wl2": dict(d=2, Nx=32, Nv=64, vmax=6.0, tau=1 / 8, N=160, bench="strong_landau_2d", alpha=0.01, keep=51),
-    "wl3": dict(d=3, Nx=16, Nv=32, vmax=6.0, tau=1 / 8, N=10, bench="weak_landau_3d", alpha=0.01, keep=11),
+    # full size to t_end (80 steps, ~3 h of numba on 8 cores); the fixture is rewritten
+    # every few steps, truncated to the steps done, so a cut-off run still pins 0..n
+    "wl3": dict(d=3, Nx=16, Nv=32, vmax=6.0, tau=1 / 8, N=80, bench="weak_landau_3d", alpha=0.01, keep=51,
+                save_every=2),
     # reduced / small cases (fast parity cases; oracle finishes in seconds)
     "wl3r": dict(d=3, Nx=16, Nv=8, vmax=6.0, tau=1 / 8, N=80, bench="weak_landau_3d", alpha=0.01, keep=81),
     "kat_wl": dict(d=1, Nx=32, Nv=128, vmax=10.0, tau=1 / 16, N=160, bench="weak_landau_1d", alpha=None, keep=161),
@@ -141,20 +144,28 @@ def run(name, cfg):
             rho[n] = r.density.values.reshape(-1)
             coeffs[n] = np.asarray(hist.entry(n).coeffs, dtype=np.float64).reshape(-1)  # the stored slab
             E[n] = kernels.eval_E_many(fit.coeffs, g.L, Xn)
-        if n % 50 == 0:
+        if cfg.get("save_every") and n % cfg["save_every"] == 0 and n < N:
+            save(name, cfg, g, ic, ctx, n, keep, rho, coeffs, E, W, stats, t_rho, t_tail, evals, t0)
+        if n % 50 == 0 or cfg.get("save_every"):
             print(f"[{name}] step {n}/{N}  W={W[n]:.6e}  t={time.time() - t0:.1f}s", flush=True)
-    np.savez_compressed(
-        os.path.join(OUT, f"{name}.npz"),
-        rho=rho, coeffs=coeffs, E=E, W=W, stats=stats, t_rho=t_rho, t_tail=t_tail,
-        field_evals=np.array(evals, dtype=np.int64), rho_bar=np.array(ctx.rho_bar),
-    )
-    meta = dict(name=name, cfg=cfg, L=g.L, ic=ic_descriptor(ic), rho_bar=ctx.rho_bar,
-                wall_s=time.time() - t0, rho_s=float(t_rho.sum()), tail_s=float(t_tail.sum()),
-                field_evals=int(ctx.field_evals), host=host_info())
-    with open(os.path.join(OUT, f"{name}.json"), "w") as fh:
-        json.dump(meta, fh, indent=1)
+    save(name, cfg, g, ic, ctx, N, keep, rho, coeffs, E, W, stats, t_rho, t_tail, evals, t0)
     print(f"[{name}] done in {time.time() - t0:.1f}s", flush=True)
     return g, ic, hist
+
+
+def save(name, cfg, g, ic, ctx, n, keep, rho, coeffs, E, W, stats, t_rho, t_tail, evals, t0):
+    """Write the fixture for steps 0..n (W/stats for every step run, rho/coeffs/E for min(keep, n+1))."""
+    k = min(keep, n + 1)
+    np.savez_compressed(
+        os.path.join(OUT, f"{name}.npz"),
+        rho=rho[:k], coeffs=coeffs[:k], E=E[:k], W=W[: n + 1], stats=stats[: n + 1], t_rho=t_rho[: n + 1],
+        t_tail=t_tail[: n + 1], field_evals=np.array(evals[: n + 1], dtype=np.int64), rho_bar=np.array(ctx.rho_bar),
+    )
+    meta = dict(name=name, cfg=cfg, steps_done=n, L=g.L, ic=ic_descriptor(ic), rho_bar=ctx.rho_bar,
+                wall_s=time.time() - t0, rho_s=float(t_rho[: n + 1].sum()), tail_s=float(t_tail[: n + 1].sum()),
+                field_evals=int(evals[n]), host=host_info())
+    with open(os.path.join(OUT, f"{name}.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
 
 
 def trace_goldens(name, g, stack, tau, n, M=2000, seed=1234):
@@ -307,6 +318,90 @@ def hook_goldens():
                             V_uniform=VU, evals=np.array(ctx.field_evals))
 
 
+API_ICS = ("weak_landau_1d", "two_stream_1d", "strong_landau_2d", "two_stream_3d", "weak_landau_3d")
+
+
+def api_goldens():
+    """The reference's module-level API beyond the loop (the drop-in surface a vpflow caller
+    imports): initial.eval_f0 / background_density (initial.py:165-208), kernels.bspline_weights
+    / bspline_dweights (kernels.py:62-81), poisson.transform_values / inverse_transform
+    (poisson.py:72-87) on seeded inputs."""
+    from vpflow import initial, kernels, poisson
+    from vpflow.grids import GridSpec
+    from vpflow.initial import InitialCondition, VelocityProfile, make_benchmark
+
+    rng = np.random.default_rng(314)
+    out = {}
+    for name in API_ICS:
+        if name == "weak_landau_3d":
+            ic = InitialCondition(benchmark=name, d=3, L=4 * math.pi, alpha=0.01, k=0.5,
+                                  profiles=(VelocityProfile(),) * 3)
+        else:
+            ic = make_benchmark(name)
+        d = ic.d
+        x = rng.uniform(-2 * ic.L, 3 * ic.L, (700, d))
+        v = rng.uniform(-9.0, 9.0, (700, d))
+        out[f"f0_{name}_x"] = x
+        out[f"f0_{name}_v"] = v
+        out[f"f0_{name}_F"] = initial.eval_f0(ic, x, v)
+        xb = rng.uniform(0, ic.L, (3, 5, d))
+        vb = rng.normal(0, 2, (3, 5, d))
+        out[f"f0b_{name}_x"] = xb
+        out[f"f0b_{name}_v"] = vb
+        out[f"f0b_{name}_F"] = initial.eval_f0(ic, xb, vb)
+    for cname in ("wl1", "ts1", "sl1", "wl2", "wl3", "wl3r", "tiny3", "rag2"):
+        g, ic = build(CONFIGS[cname])
+        out[f"rhobar_{cname}"] = np.array(initial.background_density(ic, g))
+    t = np.concatenate([rng.uniform(0, 1, 997), [0.0, 1.0, 1e-300, 1 - 1e-16, 0.5, 0.25]])
+    out["bs_t"] = t
+    out["bs_w"] = kernels.bspline_weights(t)
+    out["bs_dw"] = kernels.bspline_dweights(t)
+    t2 = rng.uniform(0, 1, (7, 9))
+    out["bs_t2"] = t2
+    out["bs_w2"] = kernels.bspline_weights(t2)
+    out["bs_dw2"] = kernels.bspline_dweights(t2)
+    for d, N in ((1, 32), (1, 5), (2, 8), (2, 6), (3, 8), (3, 5)):
+        g = GridSpec(d=d, L=4 * math.pi, Nx=N, Nv=4, vmax=6.0)
+        vals = rng.normal(0, 1, g.shape_x)
+        spec = poisson.transform_values(g, vals)
+        out[f"tr_{d}_{N}_in"] = vals
+        out[f"tr_{d}_{N}_spec"] = spec.coeffs
+        cplx = rng.normal(0, 1, g.shape_x) + 1j * rng.normal(0, 1, g.shape_x)
+        out[f"tr_{d}_{N}_cin"] = cplx
+        out[f"tr_{d}_{N}_inv"] = poisson.inverse_transform(poisson.SpectralField(grid=g, coeffs=cplx))
+    np.savez_compressed(os.path.join(OUT, "api.npz"), **out)
+
+
+def hook_spline_goldens():
+    """FlowContext.install_field(step, SplineField) (flow.py:44-47): stored slots replaced by
+    OTHER steps' spline fields (plus one UniformField), then psi_batch / psi_tilde_batch
+    through the reference's generic trace (flow.py:65-82)."""
+    from vpflow import flow, spline
+
+    for base, (n, slots) in HOOK_CASES.items():
+        g, ic = build(CONFIGS[base])
+        tau = CONFIGS[base]["tau"]
+        z = np.load(os.path.join(OUT, f"{base}.npz"))
+        stack = z["coeffs"].reshape((-1,) + (g.Nx,) * g.d)
+        hist = spline.PotentialHistory(g, tau)
+        for c in stack[: n + 1]:
+            hist.append(spline.SplineField(grid=g, coeffs=np.ascontiguousarray(c)))
+        ctx = flow.FlowContext(history=hist, ic=ic, tau=tau, grid=g)
+        rng = np.random.default_rng(2025)
+        src = [int(s) + n // 2 + 1 for s in slots]  # a later step's field in each slot
+        for s_, k in zip(slots, src):
+            ctx.install_field(s_, spline.SplineField(grid=g, coeffs=np.ascontiguousarray(stack[k])))
+        Eu = rng.uniform(-0.3, 0.3, g.d)
+        ctx.install_field(n - 1, spline.UniformField(Eu))
+        x = rng.uniform(-g.L, 2 * g.L, (300, g.d))
+        v = rng.uniform(-g.vmax, g.vmax, (300, g.d))
+        X1, V1 = flow.psi_batch(ctx, n, x, v)
+        X0, V0 = flow.psi_tilde_batch(ctx, n, x, v)
+        np.savez_compressed(os.path.join(OUT, f"hookspline_{base}.npz"), n=np.array(n), slots=np.array(slots),
+                            src=np.array(src), E_uniform=Eu, x=x, v=v, X_psi=X1, V_psi=V1, X_tilde=X0, V_tilde=V0,
+                            evals=np.array(ctx.field_evals))
+
+
 def host_info():
     try:
         cpu = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
@@ -330,6 +425,12 @@ def main(argv):
             continue
         if name == "hooks":
             hook_goldens()
+            continue
+        if name == "api":
+            api_goldens()
+            continue
+        if name == "hooks_spline":
+            hook_spline_goldens()
             continue
         if name.startswith("sweep_"):
             base = name[len("sweep_"):]

@@ -65,9 +65,13 @@ def sharded_run(name, N, world, B=8, asynchronous=False):
     return rho, W, hists, evals
 
 
-@pytest.mark.parametrize("name,N", [("kat_wl", 40), ("tiny2", 12), ("tiny3", 8), ("rag1", 20)])
+@pytest.mark.parametrize("name,N", [("kat_wl", 40), ("tiny2", 12), ("tiny3", 8), ("rag1", 20), ("ts1", 80),
+                                    ("wl1", 40), ("sl1", 16)])
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_sharded_bit_identical_to_single_gpu(name, N, world):
+    """Also on the BASELINE d = 1 grids, whose tile height the single-GPU run picks from the
+    grid (ts1 8 rows, wl1 4, sl1 16): a rank must tile the same way although it traces
+    only 1/world of the rows, else its block sums group rows differently."""
     w = workload(name)
     sim = nufi.Simulation(w.grid, w.ic, w.tau, N, v_blocks=8)
     ref = sim.run()
