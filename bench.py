@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--config", default="ts1")
     ap.add_argument("--impl", default="nufi", choices=["nufi", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-api-step", action="store_true", help="skip the per-step drop-in loop leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU sample length")
     ap.add_argument("--force-dist", action="store_true",
                     help="test hook: take the multi-rank (NCCL) code path even with one rank")
@@ -372,6 +373,38 @@ def smem_roofline(torch, dev, d, trace_ps, trace_ms):
              "(2.0 wavefronts per 8-byte warp load, ncu, profiles/); co-bound with the FP64 pipe")}
 
 
+def api_step_leg(nufi, w, dev, reps: int) -> dict:
+    """The drop-in loop a vpflow caller writes: per step
+    r = compute_rho(ctx, n); up = advance(ctx, r.density) -- the whole run to t_end,
+    wall-clocked, every step's rho / W / E / coefficients reaching the host.  Two variants:
+    W read every step (one host wait per step), and every result read after the loop (the
+    calls only enqueue; pending.py)."""
+    g = w.grid
+
+    def loop(read_each):
+        hist = nufi.PotentialHistory(g, w.tau, capacity=w.n_steps + 1, device=dev)
+        ctx = nufi.FlowContext(history=hist, ic=w.ic, tau=w.tau, grid=g)
+        t0 = time.perf_counter()
+        res = []
+        for n in range(w.n_steps + 1):
+            r = nufi.compute_rho(ctx, n)
+            up = nufi.advance(ctx, r.density)
+            if read_each:
+                _ = up.W
+            res.append((r, up))
+        for r, up in res:  # every output on the host
+            _ = (r.density.values, r.f_max, up.W, up.E)
+        return time.perf_counter() - t0
+
+    out = {}
+    for key, each in (("read_each_step", True), ("read_at_end", False)):
+        times = [loop(each) for _ in range(reps + 1)][1:]  # first pass warms up
+        t = float(np.median(times))
+        out[key] = {"value": w.point_steps / t, "wall_s_to_t_end": t}
+    return {"value": out["read_each_step"]["value"], "unit": "point-steps/s", "runs": reps, **out,
+            "api": "for n in 0..N: r = compute_rho(ctx, n); up = advance(ctx, r.density) (host outputs)"}
+
+
 def flush_l2(torch, buf):
     buf.add_(1.0)  # 256 MiB write > 126 MB L2
 
@@ -480,6 +513,12 @@ def gpu_arm(args, rank: int, world: int):
                 e2e_times.append(float(t_run.item()))
         e2e_value = args.steps * ps_run / float(np.sum(e2e_times))
 
+    # ---- the reference-shaped per-step loop: compute_rho + advance per
+    # step through the public API, host outputs, W read every step ----
+    api_step = None
+    if not dist_mode and not args.no_api_step:
+        api_step = api_step_leg(nufi, w, dev, max(1, min(args.steps, 3)))
+
     # ---- roofline: one additional identical run with per-launch CUDA events ----
     h = sim.history.handle
     lib.nufi_profiling(h.h, 1)
@@ -537,6 +576,7 @@ def gpu_arm(args, rank: int, world: int):
                     "api": ("Simulation(grid, ic, tau, N).run()" if not dist_mode else
                             "DistributedSimulation(grid, ic, tau, N).run() on every rank (max over ranks)")
                            + " -> host numpy rho/E/W/stats per time step"},
+            "api_step": api_step,
             "gpu_launches": launches_per_run * args.steps,
             "roofline": roofline,
             "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample",

@@ -202,6 +202,28 @@ int nufi_fit_spline(nufi_handle *h, const double *phi, double *coeffs_out);
 int nufi_transform_values(nufi_handle *h, const double *values, double *spec_re, double *spec_im);
 int nufi_inverse_transform(nufi_handle *h, const double *spec_re, const double *spec_im, double *values_out);
 
+/* Stream-ordered forms of the per-step drop-in pair (compute_rho + the tail), for a host
+ * loop that must not wait on every call.  nufi_async_slots allocates a ring of `slots`
+ * pinned host entries; an entry holds [rho (Nx^d) | stats3 | W | status (int32 in a
+ * double slot) | pad | E (Nx^d*d) | coeffs (Nx^d)]; the kernels write it directly (mapped
+ * pinned memory), so no copy is enqueued on the common path.  nufi_rho_async enqueues compute_rho of step n (same checks as
+ * nufi_rho) and its rho / stats copies into entry `slot`; nufi_field_update_async enqueues
+ * the tail (rho: host / device Nx^d values, or NULL = the density the last nufi_rho_async
+ * left on the device -- no copy) and its W / E / coeffs copies into entry `slot`, and
+ * advances the history length provisionally.  Neither waits.  nufi_async_wait blocks until
+ * the entry's copies are complete and returns a pointer to it (valid until the slot is
+ * reused); a non-neutral density in any enqueued tail makes it return NUFI_ERR_NUMERICAL
+ * (history length reset to the fields actually appended, later tails skipped). */
+int nufi_async_slots(nufi_handle *h, int slots);
+int nufi_rho_async(nufi_handle *h, int64_t n, int slot, int64_t *evals, int *speculative);
+/* When n == history length (the loop's next step), nufi_rho_async runs the WHOLE step in
+ * one launch -- the tail writes slot n without committing it -- and sets *speculative = 1;
+ * nufi_commit_async(h, n) then appends it (history length n + 1) with no further work.
+ * Any other call that writes the history or changes f0 discards the speculation. */
+int nufi_commit_async(nufi_handle *h, int64_t n);
+int nufi_field_update_async(nufi_handle *h, const double *rho, int slot);
+int nufi_async_wait(nufi_handle *h, int slot, double **entry);
+
 /* One full step n (requires len == n): nufi_rho + nufi_field_update, all on
  * the device.  Outputs optional. */
 int nufi_step(nufi_handle *h, int64_t n, double *rho_out, double *E_out, double *W_out,

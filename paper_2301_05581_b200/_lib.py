@@ -99,6 +99,11 @@ _SIGS = {
     "nufi_mg_step_async": [_P, _I64, _P, _P, _P, _P],
     "nufi_partials_len": [_P],
     "nufi_field_update": [_P, _P, _P, _P, _P],
+    "nufi_async_slots": [_P, ctypes.c_int],
+    "nufi_rho_async": [_P, _I64, ctypes.c_int, _I64P, ctypes.POINTER(ctypes.c_int)],
+    "nufi_commit_async": [_P, _I64],
+    "nufi_field_update_async": [_P, _P, ctypes.c_int],
+    "nufi_async_wait": [_P, ctypes.c_int, ctypes.POINTER(ctypes.POINTER(ctypes.c_double))],
     "nufi_step": [_P, _I64, _P, _P, _P, _P, _I64P],
     "nufi_run": [_P, _I64, _P, _P, _P, _P, _I64P],
     "nufi_trace": [_P, _I64, _P, _P, _I64, ctypes.c_int, ctypes.c_int, _I64P],

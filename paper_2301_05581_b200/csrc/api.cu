@@ -161,6 +161,14 @@ struct nufi_handle {
     std::map<int64_t, std::vector<double>> ovr_spline;  // installed SplineField slabs by slot
     int64_t n_ovr = 0;
 
+    // stream-ordered drop-in calls (nufi_rho_async / nufi_field_update_async): a ring of
+    // pinned host entries [rho | stats 3 | W 1 | pad | E nodes*d | coeffs nodes], one event each
+    std::vector<double *> aring;
+    std::vector<cudaEvent_t> aev;
+    size_t aslot_elems = 0;
+    bool d_rho_async = false;  // d_rho holds the density of the last nufi_rho_async
+    int64_t spec = -1;         // slot n holds a speculative (uncommitted) tail of nufi_rho_async(n)
+
     int64_t len = 0;  // host mirror of the history length
     bool large = false;   // Nx^d > MAX_FIELD_NODES: multi-CTA tail (field_large.cu)
     bool gl = false;      // slabs too large for a shared-memory ring: traced in place (GL kernels)
@@ -465,6 +473,7 @@ static int grow(nufi_handle *h, int64_t cap) {
 extern "C" {
 
 int nufi_set_initial_condition(nufi_handle *h, const nufi_config *cfg) {
+    if (h) h->spec = -1;
     CHECK_HANDLE(h);
     if (!cfg) return fail(NUFI_ERR_USAGE, "null config");
     if (cfg->d != h->cfg.d || cfg->Nx != h->cfg.Nx || cfg->Nv != h->cfg.Nv || cfg->L != h->cfg.L ||
@@ -481,6 +490,7 @@ int nufi_set_initial_condition(nufi_handle *h, const nufi_config *cfg) {
 }
 
 int nufi_reserve(nufi_handle *h, int64_t slabs) {
+    if (h) h->spec = -1;
     CHECK_HANDLE(h);
     if (slabs > (int64_t)1 << 30) return fail(NUFI_ERR_USAGE, "capacity too large");
     return grow(h, slabs);
@@ -631,6 +641,10 @@ int nufi_destroy(nufi_handle *h) {
                     (void *)h->large_scratch, (void *)h->halo})
         if (p) cudaFreeAsync(p, h->stream);
     mg_release(h);
+    for (size_t q = 0; q < h->aring.size(); ++q) {
+        pinned_put(h->aring[q], h->aslot_elems);
+        cudaEventDestroy(h->aev[q]);
+    }
     cudaStreamSynchronize(h->stream);  // frees complete -> the pool can hand the memory to the next handle
     pinned_put(h->run_host, h->run_elems);
     if (h->own_stream) cudaStreamDestroy(h->stream);
@@ -661,6 +675,7 @@ int nufi_history_len(nufi_handle *h, int64_t *len) {
 }
 
 int nufi_load_history(nufi_handle *h, const double *coeffs, int64_t count) {
+    if (h) h->spec = -1;
     CHECK_HANDLE(h);
     if (count < 0 || count > h->cap) return fail(NUFI_ERR_USAGE, "history count exceeds the capacity n_max + 1");
     if (count > 0 && !coeffs) return fail(NUFI_ERR_USAGE, "null coefficients");
@@ -687,6 +702,7 @@ int nufi_get_history(nufi_handle *h, double *coeffs, int64_t first, int64_t coun
 }
 
 int nufi_append_coeffs(nufi_handle *h, const double *coeffs) {
+    if (h) h->spec = -1;
     CHECK_HANDLE(h);
     if (!coeffs) return fail(NUFI_ERR_USAGE, "null coefficients");
     if (h->len >= h->cap) return fail(NUFI_ERR_USAGE, "history is full (capacity n_max + 1)");
@@ -700,6 +716,7 @@ int nufi_append_coeffs(nufi_handle *h, const double *coeffs) {
 }
 
 int nufi_truncate_history(nufi_handle *h, int64_t count) {
+    if (h) h->spec = -1;
     if (!h) return fail(NUFI_ERR_USAGE, "null handle");
     if (count < 0 || count > h->len) return fail(NUFI_ERR_USAGE, "truncate beyond the stored history");
     h->len = count;
@@ -831,19 +848,23 @@ static int enqueue_reduce(nufi_handle *h, int b_lo, int b_hi, double *out) {
 
 // outputs of one step (device pointers, any may be null)
 struct StepOut {
-    double *rho = nullptr, *E = nullptr, *W = nullptr, *stats = nullptr;
+    double *rho = nullptr, *E = nullptr, *W = nullptr, *stats = nullptr, *coeffs = nullptr;
+    int *status_mirror = nullptr;
 };
 
 // A whole single-rank step n: compute_rho (+ the field update tail when full).
 // d = 1: one fused launch (the last CTA runs the tail); d = 2, 3: trace ->
 // block reduce -> field_update.
 static int enqueue_step(nufi_handle *h, int64_t n, bool full, const StepOut &o) {
+    h->d_rho_async = false;
     FieldParams f = field_params(h);
     f.slot = n;
     f.rho_out = o.rho;
     f.stats_out = o.stats;
     f.W_out = o.W;
     f.E_out = o.E;
+    f.coeffs_out = o.coeffs;
+    f.status_mirror = o.status_mirror;
     f.finish_only = full ? 0 : 1;
     static const bool nofuse = getenv("NUFI_NOFUSE") != nullptr;
     if (h->d == 1 && !nofuse && !h->large) {
@@ -977,6 +998,7 @@ int nufi_rho_partials(nufi_handle *h, int64_t n, double *partials, int64_t *eval
 
 int nufi_rho_finish(nufi_handle *h, const double *partials, double *rho_out, double *stats3) {
     CHECK_HANDLE(h);
+    h->d_rho_async = false;
     if (!is_device_ptr(partials)) return fail(NUFI_ERR_USAGE, "partials must be a device buffer");
     FieldParams f = field_params(h);
     f.sums = partials;
@@ -1008,7 +1030,9 @@ int nufi_rho(nufi_handle *h, int64_t n, double *rho_out, double *stats3, int64_t
 }
 
 int nufi_field_update(nufi_handle *h, const double *rho, double *W_out, double *E_out, double *coeffs_out) {
+    if (h) h->spec = -1;
     CHECK_HANDLE(h);
+    h->d_rho_async = false;
     if (!rho) return fail(NUFI_ERR_USAGE, "null rho");
     if (h->len >= h->cap) return fail(NUFI_ERR_USAGE, "history is full (capacity n_max + 1)");
     CU(cudaMemcpyAsync(h->d_rho, rho, h->nodes * sizeof(double), cudaMemcpyDefault, h->stream));
@@ -1029,8 +1053,131 @@ int nufi_field_update(nufi_handle *h, const double *rho, double *W_out, double *
     return copy_step_outputs(h, nullptr, E_out, W_out, nullptr);
 }
 
+// ---- stream-ordered drop-in calls: outputs land in a pinned ring entry, no host sync ----
+
+// entry layout: [rho nodes | stats 3 | W 1 | status (int) 1 | pad 1 | E nodes*d | coeffs nodes]
+static size_t aslot_off_stats(const nufi_handle *h) { return (size_t)h->nodes; }
+static size_t aslot_off_W(const nufi_handle *h) { return (size_t)h->nodes + 3; }
+static size_t aslot_off_status(const nufi_handle *h) { return (size_t)h->nodes + 4; }
+static size_t aslot_off_E(const nufi_handle *h) { return (size_t)h->nodes + 6; }
+static size_t aslot_off_C(const nufi_handle *h) { return (size_t)h->nodes * (1 + h->d) + 6; }
+
+int nufi_async_slots(nufi_handle *h, int slots) {
+    CHECK_HANDLE(h);
+    if (slots < 1 || slots > 4096) return fail(NUFI_ERR_USAGE, "slots must be 1..4096");
+    CU(cudaStreamSynchronize(h->stream));
+    for (size_t q = 0; q < h->aring.size(); ++q) {
+        pinned_put(h->aring[q], h->aslot_elems);
+        cudaEventDestroy(h->aev[q]);
+    }
+    h->aring.assign(slots, nullptr);
+    h->aev.assign(slots, nullptr);
+    h->aslot_elems = (size_t)h->nodes * (2 + h->d) + 6;
+    for (int q = 0; q < slots; ++q) {
+        CU(pinned_get(&h->aring[q], h->aslot_elems));
+        CU(cudaEventCreateWithFlags(&h->aev[q], cudaEventDisableTiming));
+    }
+    return NUFI_OK;
+}
+
+static int aslot_check(nufi_handle *h, int slot) {
+    if (slot < 0 || slot >= (int)h->aring.size()) return fail(NUFI_ERR_USAGE, "async slot out of range");
+    return NUFI_OK;
+}
+
+int nufi_rho_async(nufi_handle *h, int64_t n, int slot, int64_t *evals, int *speculative) {
+    CHECK_HANDLE(h);
+    if (int rc = refuse_installed(h)) return rc;
+    if (int rc = aslot_check(h, slot)) return rc;
+    if (n < 0) return fail(NUFI_ERR_USAGE, "step index must be >= 0");
+    if (n > 0 && h->len < n) return usage_history(h, n);
+    double *e = h->aring[slot];
+    int *st_mirror = reinterpret_cast<int *>(e + aslot_off_status(h));
+    const bool spec = n == h->len && n < h->cap && !h->large;
+    StepOut o;
+    if (spec) {
+        // the loop's next step: run the whole step (compute_rho + the tail into slot n, NOT
+        // yet committed to the history length) in one launch, every output written straight
+        // into the pinned entry; advance() of this density then only commits
+        o.rho = e;
+        o.stats = e + aslot_off_stats(h);
+        o.W = e + aslot_off_W(h);
+        o.E = e + aslot_off_E(h);
+        o.coeffs = e + aslot_off_C(h);
+        o.status_mirror = st_mirror;
+        int rc = enqueue_step(h, n, true, o);
+        if (rc) return rc;
+        if (h->large) CU(cudaMemcpyAsync(st_mirror, h->d_status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        h->spec = n;
+    } else {
+        o.rho = h->d_rho;
+        o.stats = h->d_stats;
+        int rc = enqueue_step(h, n, false, o);
+        if (rc) return rc;
+        CU(cudaMemcpyAsync(e, h->d_rho, h->nodes * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CU(cudaMemcpyAsync(e + aslot_off_stats(h), h->d_stats, 3 * sizeof(double), cudaMemcpyDeviceToHost,
+                           h->stream));
+        CU(cudaMemcpyAsync(st_mirror, h->d_status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        h->d_rho_async = true;
+    }
+    CU(cudaEventRecord(h->aev[slot], h->stream));
+    if (evals) *evals += (int64_t)point_steps(h, n, h->B);
+    if (speculative) *speculative = spec ? 1 : 0;
+    return NUFI_OK;
+}
+
+int nufi_commit_async(nufi_handle *h, int64_t n) {
+    CHECK_HANDLE(h);
+    if (h->spec != n || h->len != n) return fail(NUFI_ERR_USAGE, "no speculative tail of this step to commit");
+    h->spec = -1;
+    h->len += 1;  // provisional like nufi_field_update_async
+    return NUFI_OK;
+}
+
+int nufi_field_update_async(nufi_handle *h, const double *rho, int slot) {
+    CHECK_HANDLE(h);
+    if (int rc = aslot_check(h, slot)) return rc;
+    if (h->len >= h->cap) return fail(NUFI_ERR_USAGE, "history is full (capacity n_max + 1)");
+    if (!rho && !h->d_rho_async)
+        return fail(NUFI_ERR_USAGE, "no device density: the last call that wrote one was not nufi_rho_async");
+    h->spec = -1;
+    if (rho) CU(cudaMemcpyAsync(h->d_rho, rho, h->nodes * sizeof(double), cudaMemcpyDefault, h->stream));
+    h->d_rho_async = false;
+    double *e = h->aring[slot];
+    FieldParams f = field_params(h);
+    f.rho_in = h->d_rho;  // NULL rho: the density the last nufi_rho_async left on the device
+    f.slot = h->len;
+    f.W_out = e + aslot_off_W(h);  // written straight into the pinned entry
+    f.E_out = e + aslot_off_E(h);
+    f.coeffs_out = e + aslot_off_C(h);
+    f.status_mirror = reinterpret_cast<int *>(e + aslot_off_status(h));
+    {
+        ProfScope ps(h, 2);
+        CU(enqueue_field(h, f));
+    }
+    if (h->large) CU(cudaMemcpyAsync(f.status_mirror, h->d_status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaEventRecord(h->aev[slot], h->stream));
+    h->len += 1;  // provisional; nufi_async_wait / nufi_check_status reconcile a failed step
+    return NUFI_OK;
+}
+
+int nufi_async_wait(nufi_handle *h, int slot, double **entry) {
+    CHECK_HANDLE(h);
+    if (int rc = aslot_check(h, slot)) return rc;
+    CU(cudaEventSynchronize(h->aev[slot]));
+    int st = 0;
+    memcpy(&st, h->aring[slot] + aslot_off_status(h), sizeof(int));  // the status as of this entry
+    if (st != 0) {
+        int rc = nufi_check_status(h);  // reconciles len, clears the flag, sets the message
+        if (rc) return rc;
+    }
+    if (entry) *entry = h->aring[slot];
+    return NUFI_OK;
+}
+
 int nufi_step(nufi_handle *h, int64_t n, double *rho_out, double *E_out, double *W_out, double *stats3,
               int64_t *evals) {
+    if (h) h->spec = -1;
     CHECK_HANDLE(h);
     if (int rc = refuse_installed(h)) return rc;
     if (n != h->len) {
@@ -1055,7 +1202,9 @@ int nufi_step(nufi_handle *h, int64_t n, double *rho_out, double *E_out, double 
 
 int nufi_step_finish(nufi_handle *h, int64_t n, const double *partials, double *rho_out, double *E_out,
                      double *W_out, double *stats3) {
+    if (h) h->spec = -1;
     CHECK_HANDLE(h);
+    h->d_rho_async = false;
     if (n != h->len) return fail(NUFI_ERR_USAGE, "step_finish requires len == n");
     if (n >= h->cap) return fail(NUFI_ERR_USAGE, "history is full (capacity n_max + 1)");
     if (!is_device_ptr(partials)) return fail(NUFI_ERR_USAGE, "partials must be a device buffer");
@@ -1081,7 +1230,9 @@ int nufi_step_finish(nufi_handle *h, int64_t n, const double *partials, double *
 
 int nufi_step_finish_async(nufi_handle *h, int64_t n, const double *partials, double *rho_out, double *E_out,
                            double *W_out, double *stats3) {
+    if (h) h->spec = -1;
     CHECK_HANDLE(h);
+    h->d_rho_async = false;
     if (n != h->len) return fail(NUFI_ERR_USAGE, "step_finish requires len == n");
     if (n >= h->cap) return fail(NUFI_ERR_USAGE, "history is full (capacity n_max + 1)");
     for (const void *q : {(const void *)partials, (const void *)rho_out, (const void *)E_out, (const void *)W_out,
@@ -1208,7 +1359,9 @@ int nufi_mg_handle_size(void) { return (int)sizeof(cudaIpcMemHandle_t); }
 // the same table contents as a real run.  Stream-ordered, device outputs, no host sync;
 // nufi_check_status reports a peer that never arrived (NUFI_ERR_COMM).
 int nufi_mg_step_async(nufi_handle *h, int64_t n, double *rho_out, double *E_out, double *W_out, double *stats3) {
+    if (h) h->spec = -1;
     CHECK_HANDLE(h);
+    h->d_rho_async = false;
     if (!h->mg_own || h->d == 1) return fail(NUFI_ERR_USAGE, "call nufi_mg_setup on a d >= 2 handle first");
     if (!h->mg_emulated) {
         for (int q = 0; q < h->mg_world; ++q)
@@ -1265,7 +1418,9 @@ int nufi_mg_step_async(nufi_handle *h, int64_t n, double *rho_out, double *E_out
 
 int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, double *W_hist, double *stats_hist,
              int64_t *evals) {
+    if (h) h->spec = -1;
     CHECK_HANDLE(h);
+    h->d_rho_async = false;
     if (int rc = refuse_installed(h)) return rc;
     const int64_t first = h->len;
     if (n_last < first) return NUFI_OK;

@@ -56,6 +56,7 @@ struct FieldParams {
     double *rho_out, *stats_out, *W_out, *E_out, *coeffs_out;
     double *ev_local;   // optional second destination of the evaluation slab (persistent kernel smem)
     int *status;        // NUFI_ERR_NUMERICAL when rho is not neutral
+    int *status_mirror; // optional (e.g. pinned host): *status copied here when the tail ends
     int64_t *hist_len;  // device-side history length (slot + 1)
     int finish_only;    // compute_rho only: stop after rho / stats
     int f32_hist;       // FP32 history (spline.py:118-125): stored slabs rounded to float
@@ -71,6 +72,13 @@ struct FieldParams {
     unsigned wait_target;
     int *wait_error;
 };
+
+// end of a tail launch: publish the (sticky) device status to p.status_mirror
+__device__ __forceinline__ void mirror_status(const FieldParams &p) {
+    if (!p.status_mirror) return;
+    __syncthreads();
+    if (threadIdx.x == 0) *(volatile int *)p.status_mirror = p.status ? *(volatile int *)p.status : 0;
+}
 
 #ifndef NUFI_MG_MAX
 #define NUFI_MG_MAX 8

@@ -14,7 +14,10 @@ __global__ void __launch_bounds__(1024) field_update_kernel(const FieldParams p)
     extern __shared__ __align__(16) double fsm[];
     // an earlier step of an asynchronously enqueued sequence failed (non-neutral rho):
     // leave the history untouched, like the reference which raises before appending
-    if (p.status && *(volatile int *)p.status != 0) return;
+    if (p.status && *(volatile int *)p.status != 0) {
+        mirror_status(p);
+        return;
+    }
     if (p.wait_flags) {
         __shared__ int failed;
         if (threadIdx.x == 0) {
@@ -36,9 +39,13 @@ __global__ void __launch_bounds__(1024) field_update_kernel(const FieldParams p)
             }
         }
         __syncthreads();
-        if (failed) return;
+        if (failed) {
+            mirror_status(p);
+            return;
+        }
     }
     field_update_body(p, fsm);
+    mirror_status(p);
 }
 
 // The separate reference operations of the step tail, for callers that use them one by

@@ -178,7 +178,10 @@ __global__ void __launch_bounds__(544) trace_rho_1d_kernel(const TraceRhoParams 
     __syncthreads();
     if (!is_last) return;
     __threadfence();
-    field_update_body(fp, reinterpret_cast<double *>(smem_raw));
+    // an earlier asynchronously enqueued tail failed: leave the history untouched
+    if (fp.finish_only || !fp.status || *(volatile int *)fp.status == 0)
+        field_update_body(fp, reinterpret_cast<double *>(smem_raw));
+    mirror_status(fp);
     if (threadIdx.x == 0) *ticket = 0u;
 }
 

@@ -24,42 +24,85 @@ from .grids import GridSpec, v_mid_matrix, x_node_matrix
 DEFAULT_CHUNK = 1 << 21  # density.py:27 (accepted for signature parity; the GPU path does not chunk)
 
 
-@dataclass(frozen=True)
 class DensityGrid:
-    """rho at the Nx^d nodes, row-major (poisson.py:19-32)."""
+    """rho at the Nx^d nodes, row-major (poisson.py:19-32).
 
-    grid: GridSpec
-    values: np.ndarray
+    A density returned by compute_rho is stream-ordered: its `values` are read from the
+    device the first time they are accessed (pending.py), and advance() of it needs no
+    host copy at all."""
 
-    def __post_init__(self):
-        vals = np.asarray(self.values, dtype=np.float64)
-        if vals.shape != self.grid.shape_x:
-            raise UsageError(f"values must have shape {self.grid.shape_x}, got {vals.shape}")
-        if not np.isfinite(vals).all():
-            raise UsageError("density values must be finite")
-        object.__setattr__(self, "values", vals)
+    __slots__ = ("grid", "_values", "_entry")
+
+    def __init__(self, grid: GridSpec, values=None, *, _entry=None):
+        self.grid = grid
+        self._entry = _entry
+        self._values = None
+        if _entry is None:
+            vals = np.asarray(values, dtype=np.float64)
+            if vals.shape != grid.shape_x:
+                raise UsageError(f"values must have shape {grid.shape_x}, got {vals.shape}")
+            if not np.isfinite(vals).all():
+                raise UsageError("density values must be finite")
+            self._values = vals
+
+    @property
+    def values(self) -> np.ndarray:
+        if self._values is None:
+            self._values = self._entry.materialize()["rho"].copy()  # the entry keeps the pristine copy
+        return self._values
+
+    def __repr__(self) -> str:
+        return f"DensityGrid(grid={self.grid!r}, values={self.values!r})"
 
 
-@dataclass(frozen=True)
 class RhoResult:
-    """density.py:64-69"""
+    """density.py:64-69: density, neutralization, f_min, f_max (the scalars of a
+    stream-ordered result are read on first access)."""
 
-    density: DensityGrid
-    neutralization: float
-    f_min: float
-    f_max: float
+    __slots__ = ("density", "_stats", "_entry")
+
+    def __init__(self, density: DensityGrid, neutralization: float | None = None, f_min: float | None = None,
+                 f_max: float | None = None, *, _entry=None):
+        self.density = density
+        self._entry = _entry
+        self._stats = None if _entry is not None else (neutralization, f_min, f_max)
+
+    def _s(self, i: int) -> float:
+        if self._stats is None:
+            st = self._entry.materialize()["stats"]
+            self._stats = (float(st[0]), float(st[1]), float(st[2]))
+        return self._stats[i]
+
+    neutralization = property(lambda self: self._s(0))
+    f_min = property(lambda self: self._s(1))
+    f_max = property(lambda self: self._s(2))
+
+    def __repr__(self) -> str:
+        return (f"RhoResult(density={self.density!r}, neutralization={self.neutralization!r}, "
+                f"f_min={self.f_min!r}, f_max={self.f_max!r})")
 
 
 def compute_rho(ctx: FlowContext, n: int, chunk: int = DEFAULT_CHUNK) -> RhoResult:
-    """Charge density at step n, neutralised to zero nodal mean (density.py:72-91)."""
-    grid = ctx.grid
-    rho = np.empty(grid.n_nodes)
-    stats = np.empty(3)
+    """Charge density at step n, neutralised to zero nodal mean (density.py:72-91).
+
+    Enqueued on the device (nufi_rho_async: trace + f0 + v-reduction + neutralisation);
+    the usage checks (short history) raise here, synchronously, like the reference."""
+    from .pending import Entry, ring_of
+
+    ring = ring_of(ctx.history)
+    entry = Entry(ring, "step", int(n))
     evals = ctypes.c_int64(0)
-    ctx.history.handle.call("nufi_rho", int(n), rho.ctypes.data, stats.ctypes.data, ctypes.byref(evals))
+    spec = ctypes.c_int(0)
+    try:
+        ctx.history.handle.call("nufi_rho_async", int(n), entry.slot, ctypes.byref(evals), ctypes.byref(spec))
+    except Exception:
+        entry.release()
+        raise
+    if not spec.value:
+        entry.kind = "rho"
     ctx.field_evals += int(evals.value)
-    return RhoResult(density=DensityGrid(grid=grid, values=rho.reshape(grid.shape_x)),
-                     neutralization=float(stats[0]), f_min=float(stats[1]), f_max=float(stats[2]))
+    ring.last_rho = entry
+    return RhoResult(DensityGrid(ctx.grid, _entry=entry), _entry=entry)
 
 
 # ---------------------------------------------------------------------------

@@ -56,29 +56,78 @@ class RunResult:
         return np.arange(self.first_step, self.first_step + len(self.W))
 
 
-@dataclass(frozen=True)
 class FieldUpdate:
-    W: float
-    E: np.ndarray
-    coeffs: np.ndarray
+    """W, E at the nodes and the appended coefficients of one tail (read on first access)."""
+
+    __slots__ = ("_vals", "_entry")
+
+    def __init__(self, W: float | None = None, E: np.ndarray | None = None, coeffs: np.ndarray | None = None,
+                 *, _entry=None):
+        self._entry = _entry
+        self._vals = None if _entry is not None else {"W": W, "E": E, "coeffs": coeffs}
+
+    def _get(self, key):
+        if self._vals is None:
+            self._vals = self._entry.materialize()
+        return self._vals[key]
+
+    W = property(lambda self: self._get("W"))
+    E = property(lambda self: self._get("E"))
+    coeffs = property(lambda self: self._get("coeffs"))
 
 
 def advance(ctx: FlowContext, density: DensityGrid) -> FieldUpdate:
     """solve_poisson (poisson.py:90-112) + fit_spline (spline.py:71-86) + append
     (spline.py:132-142) + electric_energy (poisson.py:115-120) + E at the nodes,
-    on the GPU.  Raises NumericalConsistencyError for a non-neutral density."""
+    enqueued on the GPU (nufi_field_update_async).  A host density is checked for
+    neutrality here with the reference's own test (poisson.py:97-104) and raises
+    NumericalConsistencyError before anything is appended; a density that compute_rho
+    left on the device is passed without a copy (its tail re-checks on the device, and a
+    failure surfaces when a later result is read)."""
+    from .errors import NumericalConsistencyError
+    from .pending import Entry, ring_of
+
     g = ctx.grid
     if density.grid != g:
         raise UsageError("density grid does not match the context grid")
     h = ctx.history
     if len(h) >= h.capacity:
         h.reserve(2 * h.capacity)
-    rho = np.ascontiguousarray(density.values, dtype=np.float64).reshape(-1)
-    W = np.empty(1)
-    E = np.empty((g.n_nodes, g.d))
-    C = np.empty(g.n_nodes)
-    h.handle.call("nufi_field_update", rho.ctypes.data, W.ctypes.data, E.ctypes.data, C.ctypes.data)
-    return FieldUpdate(W=float(W[0]), E=E, coeffs=C.reshape(g.shape_x))
+    ring = ring_of(h)
+    e = density._entry
+    if e is not None and e is ring.last_rho:
+        ring.last_rho = None
+        # unmodified values of the step compute_rho just enqueued (never read, or read and
+        # still equal to the device's output)
+        pristine = density._values is None or np.array_equal(density._values, e.materialize()["rho"])
+        if e.kind == "step" and pristine:
+            try:
+                h.handle.call("nufi_commit_async", e.n)  # its tail already ran: commit slot n
+                return FieldUpdate(_entry=e)
+            except UsageError:  # the speculation was discarded by another call
+                pass
+        elif e.kind == "rho" and pristine:
+            entry = Entry(ring, "field")
+            try:
+                h.handle.call("nufi_field_update_async", None, entry.slot)
+                return FieldUpdate(_entry=entry)
+            except UsageError:  # another call replaced the device density: pass the host values
+                entry.release()
+    vals = density.values
+    mean = float(vals.mean())
+    tol = 1e-8 * float(np.max(np.abs(vals)))
+    if abs(mean) > tol:
+        raise NumericalConsistencyError(
+            f"density is not neutral: nodal mean {mean:.3e} exceeds tolerance {tol:.3e}; "
+            "subtract the mean before solving")
+    rho = np.ascontiguousarray(vals, dtype=np.float64).reshape(-1)
+    entry = Entry(ring, "field")
+    try:
+        h.handle.call("nufi_field_update_async", rho.ctypes.data, entry.slot)
+    except Exception:
+        entry.release()
+        raise
+    return FieldUpdate(_entry=entry)
 
 
 class Simulation:

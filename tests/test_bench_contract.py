@@ -24,3 +24,14 @@ def test_reference_arm_prints_one_contract_line():
     assert d["unit"] == "point-steps/s" and d["value"] > 0 and d["higher_is_better"] is True
     assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["kind"] in ("port", "reference")
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    # the driver divides the two arms' values only when metric / unit / direction agree
+    sys.path.insert(0, ROOT)
+    import bench
+
+    assert d["metric"] == bench.METRIC
+    src = open(os.path.join(ROOT, "bench.py")).read()
+    gpu_line = src[src.index("def gpu_arm"):]
+    assert '"metric": METRIC' in gpu_line and '"unit": "point-steps/s"' in gpu_line
+    assert '"higher_is_better": True' in gpu_line
+    # ms_per_step is what one bench step actually took: K steps fit in a few minutes
+    assert d["steps"] * d["ms_per_step"] < 300e3

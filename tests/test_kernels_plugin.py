@@ -100,6 +100,8 @@ def test_solve_poisson_fit_spline_vs_reference(name):
     from tests._util import normwise
 
     g = golden(name)
+    if g is None:
+        pytest.skip("golden missing")
     w = workload(name)
     for n in (0, 1, min(5, g["rho"].shape[0] - 1)):
         rho = nufi.DensityGrid(w.grid, g["rho"][n].reshape(w.grid.shape_x))
