@@ -138,6 +138,8 @@ struct nufi_handle {
     double *d_rho = nullptr, *d_E = nullptr, *d_W = nullptr, *d_stats = nullptr, *d_rho_bar = nullptr;
     double *tables = nullptr;  // field_common.cuh constant tables: 4N + 3 Nx^d doubles
     unsigned *ticket = nullptr;  // last-CTA-done counter of the fused d = 1 step
+    unsigned *tile_cnt = nullptr;  // d >= 2 fused block reduce: node_tiles + 1 arrival counters
+    double *block_mm = nullptr;    // d >= 2 fused block reduce: (min, max) per (block, node tile)
     unsigned *barrier = nullptr;  // grid-barrier counter of the persistent d = 1 run kernel
     int *d_status = nullptr;
     int64_t *d_len = nullptr;
@@ -580,6 +582,9 @@ int nufi_create(const nufi_config *cfg, int device, void *stream, nufi_handle **
     if (c.d >= 2) {
         CU(dalloc(&h->halo, (size_t)ev_slab_raw_elems(c.d, c.Nx) * sizeof(int), h->stream));
         CU(launch_halo_table(c.d, c.Nx, h->halo, h->stream));
+        CU(dalloc(&h->tile_cnt, ((size_t)h->node_tiles + 1) * sizeof(unsigned), h->stream));
+        CU(cudaMemsetAsync(h->tile_cnt, 0, ((size_t)h->node_tiles + 1) * sizeof(unsigned), h->stream));
+        CU(dalloc(&h->block_mm, (size_t)h->B * h->node_tiles * 2 * sizeof(double), h->stream));
     }
     CU(dalloc(&h->tables, (4 * (size_t)h->N + 3 * nodes) * sizeof(double), h->stream));
     CU(dalloc(&h->ticket, sizeof(unsigned), h->stream));
@@ -638,7 +643,7 @@ int nufi_destroy(nufi_handle *h) {
                     (void *)h->d_rho, (void *)h->d_E, (void *)h->d_W, (void *)h->d_stats, (void *)h->d_rho_bar,
                     (void *)h->d_status, (void *)h->d_len, (void *)h->run_dev, (void *)h->tables,
                     (void *)h->ticket, (void *)h->barrier, (void *)h->mom_part, (void *)h->d_mom,
-                    (void *)h->large_scratch, (void *)h->halo})
+                    (void *)h->large_scratch, (void *)h->halo, (void *)h->tile_cnt, (void *)h->block_mm})
         if (p) cudaFreeAsync(p, h->stream);
     mg_release(h);
     for (size_t q = 0; q < h->aring.size(); ++q) {
@@ -846,6 +851,33 @@ static int enqueue_reduce(nufi_handle *h, int b_lo, int b_hi, double *out) {
     return NUFI_OK;
 }
 
+// trace of blocks [b_lo, b_hi) -> block table `out`: d >= 2 in ONE launch (the block reduce
+// fused into the trace kernel, same order as reduce_blocks_kernel), d = 1 trace + reduce
+static int enqueue_trace_blocks(nufi_handle *h, int64_t n, int b_lo, int b_hi, double *out) {
+    static const bool nofuse = getenv("NUFI_NOFUSE_REDUCE") != nullptr;
+    if (h->d == 1 || nofuse || !h->tile_cnt) {
+        int rc = enqueue_trace(h, n, b_lo, b_hi);
+        if (!rc) rc = enqueue_reduce(h, b_lo, b_hi, out);
+        return rc;
+    }
+    TraceRhoParams p = trace_params(h, n, b_lo);
+    p.block_out = out;
+    p.block_mm = h->block_mm;
+    p.tile_cnt = h->tile_cnt;
+    p.b_lo = b_lo;
+    p.b_hi = b_hi;
+    const int ctas = (b_hi - b_lo) * h->vt_per_block * h->node_tiles;
+    ProfScope ps(h, 0, point_steps(h, n, b_hi - b_lo));
+    if (h->gl) {
+        TraceRhoParams q = p;
+        q.passes = h->passes * h->ppt;  // one point per thread, same rows
+        CU(launch_trace_rho_global(h->d, false, h->pow2, q, h->K, ctas, h->threads, h->stream));
+    } else {
+        CU(launch_trace_rho(h->d, h->ppt, h->pow2, p, h->K, ctas, h->threads, h->stream));
+    }
+    return NUFI_OK;
+}
+
 // outputs of one step (device pointers, any may be null)
 struct StepOut {
     double *rho = nullptr, *E = nullptr, *W = nullptr, *stats = nullptr, *coeffs = nullptr;
@@ -878,8 +910,7 @@ static int enqueue_step(nufi_handle *h, int64_t n, bool full, const StepOut &o) 
         CU(launch_trace_rho_1d(p, f, 1, h->ticket, ctas, h->threads + 32, h->stream));
         return NUFI_OK;
     }
-    int rc = enqueue_trace(h, n, 0, h->B);
-    if (!rc) rc = enqueue_reduce(h, 0, h->B, h->blocks);
+    int rc = enqueue_trace_blocks(h, n, 0, h->B, h->blocks);
     if (rc) return rc;
     f.sums = h->blocks;
     f.rows_per_block = 1;
@@ -989,8 +1020,7 @@ int nufi_rho_partials(nufi_handle *h, int64_t n, double *partials, int64_t *eval
     if (n > 0 && h->len < n) return usage_history(h, n);
     if (!is_device_ptr(partials)) return fail(NUFI_ERR_USAGE, "partials must be a device buffer");
     CU(cudaMemsetAsync(partials, 0, nufi_partials_len(h) * sizeof(double), h->stream));
-    int rc = enqueue_trace(h, n, h->b_lo, h->b_hi);
-    if (!rc) rc = enqueue_reduce(h, h->b_lo, h->b_hi, partials);
+    int rc = enqueue_trace_blocks(h, n, h->b_lo, h->b_hi, partials);
     if (rc) return rc;
     if (evals) *evals += (int64_t)point_steps(h, n, h->b_hi - h->b_lo);
     return NUFI_OK;

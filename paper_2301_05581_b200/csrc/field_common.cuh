@@ -883,8 +883,17 @@ __device__ __forceinline__ void e_at_nodes(const double *c, int N, int nodes, do
 
 // The whole tail.  `sm`: field_smem_doubles(nodes, N, rows_per_block > 1) doubles of shared memory
 // (B <= 8 when rows_per_block > 1).
+__host__ __device__ inline bool field_uses_1d_body(const FieldParams &p) {
+    return p.d == 1 && p.gc != nullptr && (p.N & (p.N - 1)) == 0 && p.B <= 8;
+}
+
+// WITH_1D = false compiles the generic body only (the d >= 2 tail kernel: without the d = 1
+// body's register arrays it fits 1024 threads x 64 registers with no spills)
+template <bool WITH_1D = true>
 static __device__ __forceinline__ bool field_update_body(const FieldParams &p, double *sm) {
-    if (p.d == 1 && p.gc != nullptr && (p.N & (p.N - 1)) == 0 && p.B <= 8) return field_update_1d_body(p, sm);
+    if constexpr (WITH_1D) {
+        if (field_uses_1d_body(p)) return field_update_1d_body(p, sm);
+    }
     const int nodes = p.nodes, N = p.N, d = p.d, T = blockDim.x;
     double *re0 = sm, *im0 = re0 + nodes, *re1 = im0 + nodes, *im1 = re1 + nodes;
     double *twc = im1 + nodes, *tws = twc + N, *sb = tws + N;

@@ -10,7 +10,10 @@
 
 namespace nufi {
 
-__global__ void __launch_bounds__(1024) field_update_kernel(const FieldParams p) {
+// WITH_1D: the d = 1 power-of-two tail (CTA width = the d = 1 trace kernel's, <= 544);
+// otherwise the generic tail for up to 1024 threads
+template <bool WITH_1D>
+__global__ void __launch_bounds__(WITH_1D ? 544 : 1024) field_update_kernel(const FieldParams p) {
     extern __shared__ __align__(16) double fsm[];
     // an earlier step of an asynchronously enqueued sequence failed (non-neutral rho):
     // leave the history untouched, like the reference which raises before appending
@@ -44,7 +47,7 @@ __global__ void __launch_bounds__(1024) field_update_kernel(const FieldParams p)
             return;
         }
     }
-    field_update_body(p, fsm);
+    field_update_body<WITH_1D>(p, fsm);
     mirror_status(p);
 }
 
@@ -157,10 +160,13 @@ size_t field_update_smem_bytes(int d, int nodes, int N) {
 // nufi_run, nufi_step and the multi-rank path are bit-identical.
 cudaError_t launch_field_update(const FieldParams &p, cudaStream_t st, int threads_req) {
     const size_t smem = field_update_smem_bytes(p.d, p.nodes, p.N);
-    cudaError_t e = cudaFuncSetAttribute(field_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const bool d1 = field_uses_1d_body(p);
+    auto kern = d1 ? field_update_kernel<true> : field_update_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const int threads = threads_req > 0 ? threads_req : (p.nodes >= 1024 ? 1024 : (p.nodes >= 128 ? 512 : 256));
-    field_update_kernel<<<1, threads, smem, st>>>(p);
+    int threads = threads_req > 0 ? threads_req : (p.nodes >= 1024 ? 1024 : (p.nodes >= 128 ? 512 : 256));
+    if (d1 && threads > 544) threads = 544;
+    kern<<<1, threads, smem, st>>>(p);
     return cudaGetLastError();
 }
 

@@ -243,6 +243,14 @@ struct TraceRhoParams {
     // outputs: partial[vt][nodes], fminmax[vt * node_tiles + tile][2]
     double *partial;
     double *fminmax;
+    // d >= 2 fused block reduce (optional): the last CTA of each node tile sums its nodes'
+    // partials per block in fixed v-tile order (reduce_blocks_kernel's order) into
+    // block_out[b][node]; the last node tile reduces the per-(block, node tile) (min, max)
+    // pairs (block_mm scratch) into block_out[B * nodes + 2 b].  Blocks [b_lo, b_hi).
+    double *block_out;
+    double *block_mm;        // B * node_tiles * 2
+    unsigned *tile_cnt;      // node_tiles + 1 arrival counters (zero between launches)
+    int b_lo, b_hi;
 };
 
 // background density (field_update.cu)

@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, WIDE ? 1 : 2) run_1d_kernel(
     // of a step is consumed before its barrier), so it reuses the ring's bytes;
     // the ring is re-armed behind a proxy fence (generic writes -> async-proxy writes).
     const size_t ring_doubles = run_1d_ring_doubles(stages, SPS, SLAB, nodes, N);
-    double *ring = reinterpret_cast<double *>(smem_raw);
+    double *ring = d1_ring_base(smem_raw);  // aligned: kick1s forms addresses by OR
     double *tail = ring;                                                   // field_smem_doubles(nodes, N, true)
     uint64_t *full = reinterpret_cast<uint64_t *>(ring + ring_doubles);
     uint64_t *empty = full + stages;
@@ -178,8 +178,9 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, WIDE ? 1 : 2) run_1d_kernel(
                     wait_cyc += clock64() - tw0;
                     const double *buf = ring + (size_t)s_ring * SPS * SLAB;
                     if (NX != 0 && (it > 0 || top_cnt == SPS)) {
+                        const unsigned b32 = (unsigned)__cvta_generic_to_shared(buf);
 #pragma unroll
-                        for (int q = SPS - 1; q >= 0; --q) kick1<NX>(X, V, buf + q * SLAB, N);
+                        for (int q = SPS - 1; q >= 0; --q) kick1s<NX ? NX : 64>(X, V, b32 + q * SLAB * 8);
                     } else {
                         const int cnt = it == 0 ? top_cnt : SPS;
                         for (int q = cnt - 1; q >= 0; --q) {
@@ -427,7 +428,8 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, WIDE ? 1 : 2) run_1d_kernel(
 
 size_t run_1d_smem_bytes(const TraceRhoParams &p, int threads) {
     const int cw = threads / 32 - 1;
-    return run_1d_ring_doubles(p.stages, p.slabs_per_stage, p.ev_slab_elems, p.nodes, p.N) * sizeof(double) +
+    return D1_RING_ALIGN +
+           run_1d_ring_doubles(p.stages, p.slabs_per_stage, p.ev_slab_elems, p.nodes, p.N) * sizeof(double) +
            2 * p.stages * sizeof(uint64_t) + (3 * 32 * (size_t)cw + p.ev_slab_elems) * sizeof(double);
 }
 

@@ -181,6 +181,38 @@ __device__ __forceinline__ void kick1_folded(double &X, double &V, const double 
     V = fma(fc, t, V + A);
 }
 
+// shared-window alignment of the d = 1 slab rings: a multiple of 8 N for every N with a
+// compile-time kernel (slab = 3 N doubles: 8 N divides the slab and stage offsets too)
+constexpr unsigned D1_RING_ALIGN = 2048;
+
+// the d = 1 ring start: smem aligned up to D1_RING_ALIGN in the shared window (the
+// kernels reserve D1_RING_ALIGN extra bytes)
+__device__ __forceinline__ double *d1_ring_base(unsigned char *smem) {
+    const unsigned raw32 = (unsigned)__cvta_generic_to_shared(smem);
+    return reinterpret_cast<double *>(smem + (((raw32 + D1_RING_ALIGN - 1) & ~(D1_RING_ALIGN - 1)) - raw32));
+}
+
+// kick1 with the cell address formed by ONE 3-input LOP3: the slab's shared-window address
+// sbase is a multiple of N*8 (the ring is aligned to D1_RING_ALIGN bytes and every slab / stage
+// offset is a multiple of N*8), so base + 8*(i mod N) == ((8*i) & (8N-8)) | sbase -- the
+// add of the generic form (SHF, LOP3, IADD on the substep's dependent chain) disappears.
+template <int NX>
+__device__ __forceinline__ void kick1s(double &X, double &V, unsigned sbase) {
+    static_assert(NX > 0 && (NX & (NX - 1)) == 0, "power-of-two N");
+    const double s = X + MAGIC;
+    const double fc = X - (s - MAGIC);
+    const double XmV = X - V;
+    const unsigned lo = (unsigned)__double_as_longlong(s);
+    const unsigned addr = ((lo << 3) & (unsigned)(8 * NX - 8)) | sbase;
+    double A, B, C;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(A) : "r"(addr));
+    asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(B) : "r"(addr), "n"(8 * NX));
+    asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(C) : "r"(addr), "n"(16 * NX));
+    const double t = fma(fc, C, B);
+    X = fma(-fc, t, XmV - A);
+    V = fma(fc, t, V + A);
+}
+
 // One backward substep: drift x -= tau v, then kick through slab.
 template <int D, bool POW2, int NX = 0>
 __device__ __forceinline__ void substep(double (&X)[D], double (&V)[D], const double *__restrict__ slab,

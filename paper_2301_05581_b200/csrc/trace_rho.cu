@@ -31,6 +31,78 @@ namespace nufi {
 // (f_min, f_max) -> p.partial[cta][mom_count(D)].
 // GL = true: slabs too large for a shared-memory ring (large grids) are read in place
 // from the (L2-resident where it fits) global history instead of being staged.
+// The block reduce fused into the trace (threadfence-reduction pattern, two levels): the
+// last CTA to finish a node tile forms that tile's block sums, the last node tile the
+// block (min, max).  Same fixed order as reduce_blocks_kernel, so bit-identical to it.
+__device__ __forceinline__ void fused_block_reduce(const TraceRhoParams &p, int tile, int node, bool valid, int lane,
+                                                int warp, int warps) {
+    __shared__ unsigned last;
+    const int nblk = p.b_hi - p.b_lo, vpb = p.vt_per_block, nt = p.node_tiles;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(p.tile_cnt + tile, 1u) == (unsigned)(nblk * vpb) - 1u;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int bb = warp; bb < nblk; bb += warps) {
+        const int b = p.b_lo + bb;
+        const double *src = p.partial + (size_t)b * vpb * p.nodes + (valid ? node : 0);
+        double s = 0.0;
+        int t = 0;
+        for (; t + 8 <= vpb; t += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (size_t)(t + u) * p.nodes);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s += v[u];
+        }
+        for (; t < vpb; ++t) s += __ldcg(src + (size_t)t * p.nodes);
+        if (valid) p.block_out[(size_t)b * p.nodes + node] = s;
+        double mn = DBL_MAX, mx = -DBL_MAX;
+        for (int q = lane; q < vpb; q += 32) {
+            const size_t c = ((size_t)b * vpb + q) * nt + tile;
+            mn = fmin(mn, __ldcg(p.fminmax + 2 * c));
+            mx = fmax(mx, __ldcg(p.fminmax + 2 * c + 1));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (lane == 0) {
+            p.block_mm[2 * ((size_t)b * nt + tile)] = mn;
+            p.block_mm[2 * ((size_t)b * nt + tile) + 1] = mx;
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        p.tile_cnt[tile] = 0u;  // ready for the next launch
+        last = atomicAdd(p.tile_cnt + nt, 1u) == (unsigned)nt - 1u;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int bb = warp; bb < nblk; bb += warps) {
+        const int b = p.b_lo + bb;
+        double mn = DBL_MAX, mx = -DBL_MAX;
+        for (int q = lane; q < nt; q += 32) {
+            mn = fmin(mn, __ldcg(p.block_mm + 2 * ((size_t)b * nt + q)));
+            mx = fmax(mx, __ldcg(p.block_mm + 2 * ((size_t)b * nt + q) + 1));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (lane == 0) {
+            p.block_out[(size_t)p.B * p.nodes + 2 * b] = mn;
+            p.block_out[(size_t)p.B * p.nodes + 2 * b + 1] = mx;
+        }
+    }
+    if (threadIdx.x == 0) p.tile_cnt[nt] = 0u;
+}
+
 template <int D, int PPT, bool POW2, int NX, bool MOM, bool GL = false>
 __global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams p, const double K) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -274,6 +346,7 @@ __global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams 
             p.fminmax[2 * c + 1] = mx;
         }
     }
+    if (p.block_out) fused_block_reduce(p, tile, node, valid, lane, warp, warps);
 }
 
 // partial[vt][node] -> blocks[b][node] (fixed order over the block's v-tiles);

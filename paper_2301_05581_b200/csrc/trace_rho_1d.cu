@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(544) trace_rho_1d_kernel(const TraceRhoParams 
     const int SLAB = NX ? ev_slab_elems(1, NX) : p.ev_slab_elems;
     const int stages = p.stages;
 
-    double *ring = reinterpret_cast<double *>(smem_raw);
+    double *ring = d1_ring_base(smem_raw);  // aligned: kick1s forms addresses by OR
     uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)stages * SPS * SLAB);
     uint64_t *empty = full + stages;
     double *red = reinterpret_cast<double *>(empty + stages);  // 3 * 32 * cw
@@ -113,8 +113,9 @@ __global__ void __launch_bounds__(544) trace_rho_1d_kernel(const TraceRhoParams 
             mbar_wait(&full[s], ph);
             const double *buf = ring + (size_t)s * SPS * SLAB;
             if (NX != 0 && (it > 0 || top_cnt == SPS)) {
+                const unsigned b32 = (unsigned)__cvta_generic_to_shared(buf);
 #pragma unroll
-                for (int q = SPS - 1; q >= 0; --q) kick1d<NX>(X, V, buf + q * SLAB, N);
+                for (int q = SPS - 1; q >= 0; --q) kick1s<NX ? NX : 64>(X, V, b32 + q * SLAB * 8);
             } else {
                 const int cnt = it == 0 ? top_cnt : SPS;
                 for (int q = cnt - 1; q >= 0; --q) {
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(544) trace_rho_1d_kernel(const TraceRhoParams 
 }
 
 size_t trace_rho_1d_smem_bytes(const TraceRhoParams &p, int threads, int nodes) {
-    const size_t ring = (size_t)p.stages * p.slabs_per_stage * p.ev_slab_elems * sizeof(double) +
+    const size_t ring = D1_RING_ALIGN + (size_t)p.stages * p.slabs_per_stage * p.ev_slab_elems * sizeof(double) +
                         2 * p.stages * sizeof(uint64_t) + 3 * (size_t)(threads - 32) * sizeof(double);
     const size_t tail = (size_t)field_smem_doubles(nodes, p.N, true) * sizeof(double);
     return ring > tail ? ring : tail;
