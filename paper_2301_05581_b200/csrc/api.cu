@@ -1505,6 +1505,10 @@ int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, d
         // two-level combine when every CTA re-reading all tile partials would dominate the tail
         P.two_level = (int64_t)h->vt_total * h->nodes > 16384 ? 1 : 0;
         if (const char *e = getenv("NUFI_TWO_LEVEL")) P.two_level = atoi(e);
+        // next-step ring prefetch: every ring stage must hold the tail workspace
+        P.prefetch = h->stages >= 2 &&
+                     (int64_t)h->sps * h->ev_elems >= (int64_t)field_smem_doubles(h->nodes, h->N, true) &&
+                     !getenv("NUFI_NOPREFETCH");
         if (h->mg_world > 1) {
             if (!h->mg_emulated)
                 for (int q = 0; q < h->mg_world; ++q)

@@ -95,6 +95,8 @@ struct Run1DParams {
     unsigned long long *stamps;                       // optional: CTA 0 globaltimer per step x 3
     double *blocks;   // two-level combine: B * nodes block sums + B (min, max)
     int two_level;    // combine tile partials across the grid first (second grid barrier)
+    int prefetch;     // issue the next step's first ring group before this step's tail (the
+                      // tail then works in another ring stage); needs stage >= tail workspace
     // ---- multi-rank run with the exchange fused into the kernel (run_1d.cu) ----
     int mg_ranks;          // G ranks (1: single GPU)
     int mg_emulated;       // 1: the G ranks are CTA groups of this one cooperative launch

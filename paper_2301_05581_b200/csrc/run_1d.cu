@@ -122,6 +122,12 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, WIDE ? 1 : 2) run_1d_kernel(
     uint32_t ph_ring = 0;
     int fills = 0;
     unsigned gen = 0;
+    // groups consumed so far by this CTA (uniform over its threads): the ring stage the next
+    // group lands in is gsum % stages
+    long long gsum = 0;
+    const int my_tiles = lc < tiles_r ? (tiles_r - lc + nct - 1) / nct : 0;
+    const size_t stage_doubles = (size_t)SPS * SLAB;
+    bool pref_ready = false;  // this step's first group was issued before the previous tail
 
     for (int n = P.n_first; n <= P.n_last; ++n) {
         const int m = n >= 1 ? n - 1 : 0;  // slabs streamed by TMA: m-1 .. 0
@@ -132,8 +138,11 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, WIDE ? 1 : 2) run_1d_kernel(
         double *fmm = my_fminmax + (size_t)(n & 1) * P.tiles * 2;
         const int top_cnt = m - (groups - 1) * SPS;
 
+        const bool pref_now = pref_ready;
+        pref_ready = false;
         for (int t_loc = lc; t_loc < tiles_r; t_loc += nct) {
             const int tile = tile_lo + t_loc;
+            const bool first_tile = t_loc == lc;
             static constexpr bool kAlt = false;  // tile mapping: v-tile-major (true) or node-tile-major
             const int vts = P.tiles / p.node_tiles;
             const int nt = kAlt ? tile / vts : tile % p.node_tiles;
@@ -141,20 +150,23 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, WIDE ? 1 : 2) run_1d_kernel(
             const int node = nt * 32 + lane;
             double acc = 0.0, fmn = DBL_MAX, fmx = -DBL_MAX;
             if (producer) {
+                const int it0 = (pref_now && first_tile) ? 1 : 0;  // group 0 already in flight
                 if (lane == 0) {
-                    for (int it = 0; it < groups; ++it) {
+                    auto issue = [&](int g, int mm) {
                         if (fills >= stages) mbar_wait(&empty[s_ring], ph_ring ^ 1u);
-                        const int k_lo = (groups - 1 - it) * SPS, k_hi = min(m - 1, k_lo + SPS - 1);
+                        const int gg = (mm + SPS - 1) / SPS;
+                        const int k_lo = (gg - 1 - g) * SPS, k_hi = min(mm - 1, k_lo + SPS - 1);
                         const uint32_t bytes = (uint32_t)((k_hi - k_lo + 1) * SLAB * sizeof(double));
                         mbar_arrive_expect_tx(&full[s_ring], bytes);
                         tma_bulk_g2s(ring + (size_t)s_ring * SPS * SLAB, p.ev_hist + (size_t)k_lo * SLAB, bytes,
                                      &full[s_ring]);
                         ++fills;
                         if (++s_ring == stages) s_ring = 0, ph_ring ^= 1u;
-                    }
+                    };
+                    for (int it = it0; it < groups; ++it) issue(it, m);
                 } else {
                     // keep the warp's copy of the ring state in step with lane 0
-                    for (int it = 0; it < groups; ++it) {
+                    for (int it = it0; it < groups; ++it) {
                         ++fills;
                         if (++s_ring == stages) s_ring = 0, ph_ring ^= 1u;
                     }
@@ -237,6 +249,8 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, WIDE ? 1 : 2) run_1d_kernel(
             __syncthreads();
         }
 
+        gsum += (long long)my_tiles * groups;
+        pref_ready = P.prefetch && my_tiles > 0 && n < P.n_last && n >= 1;  // (groups_next > 0 iff n >= 1)
         // all partials of step n are written
         if (P.stamps && blockIdx.x == 0 && threadIdx.x == 0) P.stamps[3 * (n - P.n_first)] = globaltimer();
         if (P.stamps && threadIdx.x == 0 && (n % 400) == 0 && n > 0 && n / 400 <= 4 && blockIdx.x < 1024) {
@@ -399,10 +413,34 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, WIDE ? 1 : 2) run_1d_kernel(
             fp.mm_per_block = 1;
         }
 
+        // The next step's newest ring group (slabs n-1 .. ; slab n-1 became visible with this
+        // step's barrier) is issued now, so its copy overlaps the tail, which then works in
+        // another ring stage.
+        if (pref_ready && producer) {
+            if (lane == 0) {
+                if (fills >= stages) mbar_wait(&empty[s_ring], ph_ring ^ 1u);  // released before the barrier
+                const int gg = (n + SPS - 1) / SPS;  // step n + 1 streams slabs n - 1 .. 0
+                const int k_lo = (gg - 1) * SPS, k_hi = min(n - 1, k_lo + SPS - 1);
+                const uint32_t bytes = (uint32_t)((k_hi - k_lo + 1) * SLAB * sizeof(double));
+                mbar_arrive_expect_tx(&full[s_ring], bytes);
+                tma_bulk_g2s(ring + (size_t)s_ring * SPS * SLAB, p.ev_hist + (size_t)k_lo * SLAB, bytes,
+                             &full[s_ring]);
+            }
+            ++fills;
+            if (++s_ring == stages) s_ring = 0, ph_ring ^= 1u;
+        }
+
         // redundant tail in every CTA; CTA 0 publishes
         fp.slot = n;
         fp.ev_local = slabN;
-        fp.stage_cap = (int64_t)ring_doubles - field_smem_doubles(nodes, N, true);  // rest of the ring
+        double *tail_ws = tail;
+        if (pref_ready) {
+            // the next step's first group is landing in stage gsum % stages: work in the next one
+            tail_ws = ring + (size_t)((gsum + 1) % stages) * stage_doubles;
+            fp.stage_cap = (int64_t)stage_doubles - field_smem_doubles(nodes, N, true);
+        } else {
+            fp.stage_cap = (int64_t)ring_doubles - field_smem_doubles(nodes, N, true);  // rest of the ring
+        }
         const int64_t row = n - P.n_first;
         if (lc == 0 && !(emu && rk != 0)) {  // one publisher per rank (emulated: rank 0 only)
             fp.rho_out = P.rho_hist ? P.rho_hist + row * nodes : nullptr;
@@ -416,13 +454,17 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, WIDE ? 1 : 2) run_1d_kernel(
             fp.status = nullptr;
         }
         fp.tstamps = (P.stamps && blockIdx.x == 0 && n == P.n_last) ? P.stamps + 3 * (P.n_last - P.n_first + 1) : nullptr;
-        const bool ok = field_update_body(fp, tail);
+        const bool ok = field_update_body(fp, tail_ws);
         __syncthreads();
         // the tail's generic-proxy writes to the ring bytes must be ordered before the
         // next step's bulk copies (async proxy) into them
         if (producer && lane == 0) fence_proxy_async_smem();
         if (P.stamps && blockIdx.x == 0 && threadIdx.x == 0) P.stamps[3 * (n - P.n_first) + 2] = globaltimer();
-        if (!ok) break;  // identical decision in every CTA
+        if (!ok) {  // identical decision in every CTA
+            // no CTA may exit with the prefetched bulk copy still landing in its shared memory
+            if (pref_ready && warp == 0 && lane == 0) mbar_wait(&full[s_ring], ph_ring);
+            break;
+        }
     }
 }
 
