@@ -137,15 +137,21 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// CTA-wide sum in a fixed order (deterministic for a fixed blockDim).
+// CTA-wide sum in a fixed order (deterministic for a fixed blockDim): warp xor-trees, then
+// warp 0 combines the per-warp values with one more xor-tree (one thread per warp value
+// instead of every thread looping over all warps).
 __device__ __forceinline__ double cta_sum(double v, double *scratch) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     v = warp_sum(v);
     __syncthreads();
     if (lane == 0) scratch[warp] = v;
     __syncthreads();
-    double s = 0.0;
-    for (int w = 0; w < nw; ++w) s += scratch[w];
+    if (warp == 0) {
+        const double s = warp_sum(lane < nw ? scratch[lane] : 0.0);
+        if (lane == 0) scratch[96] = s;
+    }
+    __syncthreads();
+    const double s = scratch[96];
     __syncthreads();
     return s;
 }
@@ -157,14 +163,20 @@ __device__ __forceinline__ double cta_max(double v, double *scratch) {
     __syncthreads();
     if (lane == 0) scratch[warp] = v;
     __syncthreads();
-    double s = -DBL_MAX;
-    for (int w = 0; w < nw; ++w) s = fmax(s, scratch[w]);
+    if (warp == 0) {
+        double s = lane < nw ? scratch[lane] : -DBL_MAX;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
+        if (lane == 0) scratch[96] = s;
+    }
+    __syncthreads();
+    const double s = scratch[96];
     __syncthreads();
     return s;
 }
 
-// sum, min and max over the CTA with one shared-memory round trip (the sum in the
-// order of cta_sum: warp xor-tree, then warps in order); every thread gets the results
+// sum, min and max over the CTA with one shared-memory round trip (the sum in the order of
+// cta_sum); every thread gets the results
 __device__ __forceinline__ void cta_sum_min_max(double s, double mn, double mx, double *scratch, double &S,
                                                 double &MN, double &MX) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -181,16 +193,27 @@ __device__ __forceinline__ void cta_sum_min_max(double s, double mn, double mx, 
         scratch[64 + warp] = mx;
     }
     __syncthreads();
-    double a = 0.0, b = DBL_MAX, c = -DBL_MAX;
-    for (int w = 0; w < nw; ++w) {
-        a += scratch[w];
-        b = fmin(b, scratch[32 + w]);
-        c = fmax(c, scratch[64 + w]);
+    if (warp == 0) {
+        double a = lane < nw ? scratch[lane] : 0.0;
+        double b = lane < nw ? scratch[32 + lane] : DBL_MAX;
+        double c = lane < nw ? scratch[64 + lane] : -DBL_MAX;
+        a = warp_sum(a);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            b = fmin(b, __shfl_xor_sync(0xffffffffu, b, o));
+            c = fmax(c, __shfl_xor_sync(0xffffffffu, c, o));
+        }
+        if (lane == 0) {
+            scratch[96] = a;
+            scratch[97] = b;
+            scratch[98] = c;
+        }
     }
     __syncthreads();
-    S = a;
-    MN = b;
-    MX = c;
+    S = scratch[96];
+    MN = scratch[97];
+    MX = scratch[98];
+    __syncthreads();
 }
 
 // One separable DFT pass along the axis of stride st:
@@ -273,6 +296,79 @@ __device__ __forceinline__ void fft_axis_pass(const double *__restrict__ ire, co
         }
         __syncthreads();
     }
+}
+
+// One separable FFT along the axis of stride st = 2^logst (N = 2^logN), Stockham autosort
+// (no bit-reversal pass): one radix-2 stage when logN is odd, then radix-4 stages, each a
+// shared-memory ping-pong between (ar, ai) and (br, bi) with one CTA barrier -- log4 N + 1
+// passes over the data instead of log2 N + 1.  Same transform as fft_axis_pass:
+// out[.. alpha ..] = sum_x in[.. x ..] e^{sign 2 pi i alpha x / N}.  On return (ar, ai)
+// hold the result (the pointers are swapped once per stage).
+__device__ __forceinline__ void fft_axis_stockham(double *&ar, double *&ai, double *&br, double *&bi,
+                                                  const double *__restrict__ twc, const double *__restrict__ tws,
+                                                  int logN, int nodes, int logst, double sign) {
+    const int T = blockDim.x, N = 1 << logN;
+    int lognc = logN, logs = 0;  // current sub-transform length 2^lognc, stride 2^logs
+    while (lognc > 0) {
+        const int logr = (lognc & 1) ? 1 : 2;  // radix 2 first when log2 N is odd, then radix 4
+        const int logm = lognc - logr;
+        const int nb = nodes >> logr;  // butterflies of this stage
+        const int tshift = logN - lognc;  // twiddle index = p * N / ncur
+        for (int b = threadIdx.x; b < nb; b += T) {
+            int inner = 0, rest = b;
+            if (logst) {
+                inner = b & ((1 << logst) - 1);
+                rest = b >> logst;
+            }
+            const int q = rest & ((1 << logs) - 1);
+            const int pp = (rest >> logs) & ((1 << logm) - 1);
+            const int outer = rest >> (logs + logm);
+            const int base = (outer << (logst + logN)) + inner;
+            const int ix = base + ((q + (pp << logs)) << logst);    // x = q + s p
+            const int ox = base + ((q + (pp << (logs + logr))) << logst);  // y = q + s r p
+            const int mst = 1 << (logm + logs + logst);   // input step  s m  (in elements)
+            const int sst = 1 << (logs + logst);          // output step s
+            const int tw = pp << tshift;
+            if (logr == 1) {
+                const double a_r = ar[ix], a_i = ai[ix], b_r = ar[ix + mst], b_i = ai[ix + mst];
+                const double wr = twc[tw], wi = sign * tws[tw];
+                const double dr = a_r - b_r, di = a_i - b_i;
+                br[ox] = a_r + b_r;
+                bi[ox] = a_i + b_i;
+                br[ox + sst] = fma(dr, wr, -di * wi);
+                bi[ox + sst] = fma(dr, wi, di * wr);
+            } else {
+                const double a_r = ar[ix], a_i = ai[ix];
+                const double b_r = ar[ix + mst], b_i = ai[ix + mst];
+                const double c_r = ar[ix + 2 * mst], c_i = ai[ix + 2 * mst];
+                const double d_r = ar[ix + 3 * mst], d_i = ai[ix + 3 * mst];
+                const double w1r = twc[tw], w1i = sign * tws[tw];
+                const double w2r = twc[2 * tw], w2i = sign * tws[2 * tw];
+                const double w3r = twc[3 * tw], w3i = sign * tws[3 * tw];
+                const double apc_r = a_r + c_r, apc_i = a_i + c_i, amc_r = a_r - c_r, amc_i = a_i - c_i;
+                const double bpd_r = b_r + d_r, bpd_i = b_i + d_i;
+                // j (b - d) with j = sign * i
+                const double jb_r = -sign * (b_i - d_i), jb_i = sign * (b_r - d_r);
+                br[ox] = apc_r + bpd_r;
+                bi[ox] = apc_i + bpd_i;
+                const double x1r = amc_r + jb_r, x1i = amc_i + jb_i;
+                const double x2r = apc_r - bpd_r, x2i = apc_i - bpd_i;
+                const double x3r = amc_r - jb_r, x3i = amc_i - jb_i;
+                br[ox + sst] = fma(x1r, w1r, -x1i * w1i);
+                bi[ox + sst] = fma(x1r, w1i, x1i * w1r);
+                br[ox + 2 * sst] = fma(x2r, w2r, -x2i * w2i);
+                bi[ox + 2 * sst] = fma(x2r, w2i, x2i * w2r);
+                br[ox + 3 * sst] = fma(x3r, w3r, -x3i * w3i);
+                bi[ox + 3 * sst] = fma(x3r, w3i, x3i * w3r);
+            }
+        }
+        __syncthreads();
+        double *tr = ar, *ti = ai;
+        ar = br, ai = bi, br = tr, bi = ti;
+        lognc = logm;
+        logs += logr;
+    }
+    (void)N;
 }
 
 // In-place radix-2 complex FFT of length N = 2^logN on shared arrays (re, im) whose
@@ -909,6 +1005,7 @@ static __device__ __forceinline__ bool field_update_body(const FieldParams &p, d
 
     // ---- rho: fixed-order combine of the v-sums (density.py:80-81), neutralise (:84-85) ----
     double neut = 0.0, fmn = 0.0, fmx = 0.0;
+    double chk_s = 0.0, chk_m = 0.0;
     if (p.sums) {
         // per-block sums over the block's rows in order (same order as
         // reduce_blocks_kernel), all (block, node) items in parallel, loads batched
@@ -933,12 +1030,40 @@ static __device__ __forceinline__ bool field_update_body(const FieldParams &p, d
         }
         NUFI_STAMP(p, 1);
         double local = 0.0;
-        for (int i = threadIdx.x; i < nodes; i += T) {
-            double S = 0.0;
-            for (int b = 0; b < p.B; ++b) S += rpb > 1 ? sb[b * nodes + i] : __ldcg(p.sums + (size_t)b * nodes + i);
-            const double r = p.rho_bar - p.hv_d * S;
-            re1[i] = r;
-            local += r;
+        if (rpb == 1 && p.B <= 8) {
+            // every block sum of 2 nodes requested before any is added (one L2 round trip
+            // instead of one per block), then added in block order
+            for (int i0 = threadIdx.x; i0 < nodes; i0 += 2 * T) {
+                double v[2][8];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int i = i0 + u * T;
+#pragma unroll
+                    for (int b = 0; b < 8; ++b)
+                        v[u][b] = (i < nodes && b < p.B) ? __ldcg(p.sums + (size_t)b * nodes + i) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int i = i0 + u * T;
+                    double S = 0.0;
+#pragma unroll
+                    for (int b = 0; b < 8; ++b)
+                        if (b < p.B) S += v[u][b];
+                    if (i < nodes) {
+                        const double r = p.rho_bar - p.hv_d * S;
+                        re1[i] = r;
+                        local += r;
+                    }
+                }
+            }
+        } else {
+            for (int i = threadIdx.x; i < nodes; i += T) {
+                double S = 0.0;
+                for (int b = 0; b < p.B; ++b) S += rpb > 1 ? sb[b * nodes + i] : __ldcg(p.sums + (size_t)b * nodes + i);
+                const double r = p.rho_bar - p.hv_d * S;
+                re1[i] = r;
+                local += r;
+            }
         }
         double mn = DBL_MAX, mx = -DBL_MAX;
         const int mrows = p.B * p.mm_per_block;
@@ -948,15 +1073,21 @@ static __device__ __forceinline__ bool field_update_body(const FieldParams &p, d
         }
         double tot;
         cta_sum_min_max(local, mn, mx, scratch, tot, fmn, fmx);
-        neut = tot / (double)nodes;
+        neut = (nodes & (nodes - 1)) == 0 ? tot * (1.0 / (double)nodes) : tot / (double)nodes;  // exact for 2^k
         for (int i = threadIdx.x; i < nodes; i += T) {
-            re0[i] = re1[i] - neut;
+            const double v = re1[i] - neut;
+            re0[i] = v;
             im0[i] = 0.0;
+            chk_s += v;  // the neutrality check's partials, in its order (poisson.py:97-104)
+            chk_m = fmax(chk_m, fabs(v));
         }
     } else {
         for (int i = threadIdx.x; i < nodes; i += T) {
-            re0[i] = p.rho_in[i];
+            const double v = p.rho_in[i];
+            re0[i] = v;
             im0[i] = 0.0;
+            chk_s += v;
+            chk_m = fmax(chk_m, fabs(v));
         }
     }
     __syncthreads();
@@ -970,16 +1101,11 @@ static __device__ __forceinline__ bool field_update_body(const FieldParams &p, d
     if (p.finish_only) return true;
     NUFI_STAMP(p, 2);
 
-    // ---- neutrality check (poisson.py:97-104) ----
+    // ---- neutrality check (poisson.py:97-104), partials formed with rho' above ----
     {
-        double s = 0.0, mx = 0.0;
-        for (int i = threadIdx.x; i < nodes; i += T) {
-            s += re0[i];
-            mx = fmax(mx, fabs(re0[i]));
-        }
         double tot, unused, m;
-        cta_sum_min_max(s, DBL_MAX, mx, scratch, tot, unused, m);
-        const double mean = tot / (double)nodes;
+        cta_sum_min_max(chk_s, DBL_MAX, chk_m, scratch, tot, unused, m);
+        const double mean = (nodes & (nodes - 1)) == 0 ? tot * (1.0 / (double)nodes) : tot / (double)nodes;
         const double tol = 1e-8 * m;
         if (fabs(mean) > tol) {
             if (threadIdx.x == 0 && p.status) *p.status = NUFI_ERR_NUMERICAL;
@@ -997,10 +1123,11 @@ static __device__ __forceinline__ bool field_update_body(const FieldParams &p, d
     for (int axis = d - 1; axis >= 0; --axis) {
         int st = 1;
         for (int a = axis + 1; a < d; ++a) st *= N;
-        if (pow2)
-            fft_axis_pass(ar, ai, br, bi, twc, tws, N, 31 - __clz(N), nodes, st, -1.0);
-        else
-            dft_pass(ar, ai, br, bi, twc, tws, N, nodes, st, -1.0, G, pow2);
+        if (pow2) {
+            fft_axis_stockham(ar, ai, br, bi, twc, tws, 31 - __clz(N), nodes, 31 - __clz(st), -1.0);
+            continue;  // (ar, ai) already hold the result
+        }
+        dft_pass(ar, ai, br, bi, twc, tws, N, nodes, st, -1.0, G, pow2);
         double *tr = ar, *ti = ai;
         ar = br, ai = bi, br = tr, bi = ti;
     }
@@ -1026,10 +1153,11 @@ static __device__ __forceinline__ bool field_update_body(const FieldParams &p, d
     for (int axis = d - 1; axis >= 0; --axis) {
         int st = 1;
         for (int a = axis + 1; a < d; ++a) st *= N;
-        if (pow2)
-            fft_axis_pass(ar, ai, br, bi, twc, tws, N, 31 - __clz(N), nodes, st, 1.0);
-        else
-            dft_pass(ar, ai, br, bi, twc, tws, N, nodes, st, 1.0, G, pow2);
+        if (pow2) {
+            fft_axis_stockham(ar, ai, br, bi, twc, tws, 31 - __clz(N), nodes, 31 - __clz(st), 1.0);
+            continue;
+        }
+        dft_pass(ar, ai, br, bi, twc, tws, N, nodes, st, 1.0, G, pow2);
         double *tr = ar, *ti = ai;
         ar = br, ai = bi, br = tr, bi = ti;
     }

@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(1024) poisson_fit_kernel(FieldParams p, int mo
 
 cudaError_t launch_poisson_fit(const FieldParams &p, int mode, const double *in, double *out, double *spec_re,
                                double *spec_im, double *W, int *status, cudaStream_t st) {
-    const size_t smem = (4 * (size_t)p.nodes + 2 * p.N + 64) * sizeof(double);
+    const size_t smem = (4 * (size_t)p.nodes + 2 * p.N + 128) * sizeof(double);  // scratch: cta_sum uses 97
     cudaError_t e = cudaFuncSetAttribute(poisson_fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int threads = p.nodes >= 1024 ? 1024 : (p.nodes >= 128 ? 512 : 256);
@@ -283,7 +283,7 @@ cudaError_t launch_build_ev_slabs(double *hist, double *ev_hist, int d, int N, i
 
 
 __global__ void __launch_bounds__(1024) rho_bar_kernel(const RhoBarParams p) {
-    __shared__ double scratch[32];
+    __shared__ double scratch[128];  // cta_sum: 32 warp slots + result slot 96
     int64_t V = 1, X = 1;
     for (int a = 0; a < p.d; ++a) {
         V *= p.Nv;
