@@ -145,8 +145,9 @@ class ReferenceTimer:
     t(n) = a + b*n to extrapolate the whole run to t_end.
 
     The history is the reference's own PotentialHistory holding the golden slabs of this
-    config (steps 0..50 of the unmodified reference, tests/golden) repeated up to step N:
-    the numba trace's cost does not depend on the coefficient values.  Grids whose full
+    config (steps 0..50 of the unmodified reference, tests/golden; wl3 may use the wl3r
+    slabs, same 16^3 x-grid) repeated up to step N: the numba trace's cost does not depend
+    on the coefficient values.  Grids whose full
     compute_rho at step N would exceed ~2.5e9 point-steps (wl3) take the survey's plan:
     a = compute_rho at n = 0 on the full grid (f0 + copies + reduce, measured once),
     b from trace_backward on a node slice at the sample steps."""
@@ -173,7 +174,11 @@ class ReferenceTimer:
                                              for p in w.ic.profiles))
         self.g = g
         N = w.n_steps
-        z = np.load(os.path.join(ROOT, "tests", "golden", f"{name}.npz"))
+        # any reference history on the same x-grid will do (the trace cost is value-independent):
+        # the config's own golden, else the reduced-velocity golden of the same Nx^d
+        src = [f for f in (name, {"wl3": "wl3r"}.get(name)) if f and
+               os.path.exists(os.path.join(ROOT, "tests", "golden", f"{f}.npz"))]
+        z = np.load(os.path.join(ROOT, "tests", "golden", f"{src[0]}.npz"))
         slabs = z["coeffs"].reshape((-1,) + g.shape_x)
         hist = spline.PotentialHistory(g, w.tau)
         for m in range(N + 1):
@@ -517,7 +522,8 @@ def gpu_arm(args, rank: int, world: int):
     # step through the public API, host outputs, W read every step ----
     api_step = None
     if not dist_mode and not args.no_api_step:
-        api_step = api_step_leg(nufi, w, dev, max(1, min(args.steps, 3)))
+        reps = 1 if w.point_steps > 1e11 else max(1, min(args.steps, 3))  # wl3: one pass of each (~9 s)
+        api_step = api_step_leg(nufi, w, dev, reps)
 
     # ---- roofline: one additional identical run with per-launch CUDA events ----
     h = sim.history.handle
