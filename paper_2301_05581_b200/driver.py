@@ -88,11 +88,9 @@ def advance(ctx: FlowContext, density: DensityGrid) -> FieldUpdate:
     from .pending import Entry, ring_of
 
     g = ctx.grid
-    if density.grid != g:
+    if density.grid is not g and density.grid != g:
         raise UsageError("density grid does not match the context grid")
     h = ctx.history
-    if len(h) >= h.capacity:
-        h.reserve(2 * h.capacity)
     ring = ring_of(h)
     e = density._entry
     if e is not None and e is ring.last_rho:
@@ -113,6 +111,8 @@ def advance(ctx: FlowContext, density: DensityGrid) -> FieldUpdate:
                 return FieldUpdate(_entry=entry)
             except UsageError:  # another call replaced the device density: pass the host values
                 entry.release()
+    if len(h) >= h.capacity:
+        h.reserve(2 * h.capacity)  # PotentialHistory grows by doubling (spline.py:136-139)
     vals = density.values
     mean = float(vals.mean())
     tol = 1e-8 * float(np.max(np.abs(vals)))

@@ -83,15 +83,16 @@ class Entry:
             raise
         g = ring.history.grid
         nodes, d = g.n_nodes, g.d
-        flat = np.ctypeslib.as_array(ptr, shape=(nodes * (2 + d) + 6,))
+        # one copy of the whole entry out of the pinned ring; the fields are views of it
+        flat = np.ctypeslib.as_array(ptr, shape=(nodes * (2 + d) + 6,)).copy()
         data = {}
         if self.kind in ("rho", "step"):
-            data["rho"] = flat[:nodes].reshape(g.shape_x).copy()
-            data["stats"] = flat[nodes:nodes + 3].copy()
+            data["rho"] = flat[:nodes].reshape(g.shape_x)
+            data["stats"] = flat[nodes:nodes + 3]
         if self.kind in ("field", "step"):
             data["W"] = float(flat[nodes + 3])
-            data["E"] = flat[nodes + 6:nodes * (1 + d) + 6].reshape(nodes, d).copy()
-            data["coeffs"] = flat[nodes * (1 + d) + 6:nodes * (2 + d) + 6].reshape(g.shape_x).copy()
+            data["E"] = flat[nodes + 6:nodes * (1 + d) + 6].reshape(nodes, d)
+            data["coeffs"] = flat[nodes * (1 + d) + 6:nodes * (2 + d) + 6].reshape(g.shape_x)
         self._data = data
         if ring.owner[self.slot] is self:
             ring.owner[self.slot] = None
