@@ -68,8 +68,11 @@ __host__ __device__ inline size_t run_1d_ring_doubles(int stages, int sps, int s
 }
 
 // WIDE: 16 tracing warps + producer in one CTA per SM (experiment knob NUFI_D1_WARPS=16)
+// N = 32, 64 run one CTA per SM (the 2 x 64-slab ring fills the SM's shared memory), so their
+// register budget is not halved for a second resident CTA
 template <int NX, int SPS, int WIDE = 0>
-__global__ void __launch_bounds__(WIDE ? 544 : 288, WIDE ? 1 : 2) run_1d_kernel(const Run1DParams P) {
+__global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 32) ? 1 : 2)
+    run_1d_kernel(const Run1DParams P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const TraceRhoParams &p = P.tp;
     // warps [0, cw) trace (cw = tile rows), the last warp is the TMA producer, any
@@ -227,14 +230,20 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, WIDE ? 1 : 2) run_1d_kernel(
                 red[64 * cw + threadIdx.x] = fmx;
             }
             __syncthreads();
+            // fixed-order CTA v-sum in warp 0 (on the critical path to the barrier), the sampled
+            // (min, max) in another warp alongside
+            const int mmw = cw > 1 ? 1 : 0;
             if (warp == 0) {
-                double sum = 0.0, mn = DBL_MAX, mx = -DBL_MAX;
+                double sum = 0.0;
+                for (int w = 0; w < cw; ++w) sum += red[w * 32 + lane];
+                if (node < nodes) part[(size_t)vt * nodes + node] = sum;
+            }
+            if (warp == mmw) {
+                double mn = DBL_MAX, mx = -DBL_MAX;
                 for (int w = 0; w < cw; ++w) {
-                    sum += red[w * 32 + lane];
                     mn = fmin(mn, red[32 * cw + w * 32 + lane]);
                     mx = fmax(mx, red[64 * cw + w * 32 + lane]);
                 }
-                if (node < nodes) part[(size_t)vt * nodes + node] = sum;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
                     mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
