@@ -161,6 +161,7 @@ class DistributedSimulation:
             h.call("nufi_mg_setup", self.world, self.rank, 0, buf)
         except Exception as exc:  # pragma: no cover - depends on the machine's peer access
             ok, why = 0, exc
+        set_up = ok == 1  # this rank holds multi-rank resources to release on a fallback
         # NCCL gathers device tensors; gloo (CPU-side test groups) gathers host tensors
         where = f"cuda:{device}" if self.dist.get_backend(self.group) == "nccl" else "cpu"
         mine = t.tensor([ok] + list(buf.raw), dtype=t.uint8, device=where)
@@ -181,7 +182,7 @@ class DistributedSimulation:
         if not self.fused:
             warnings.warn(f"fused multi-rank kernel unavailable ({why or 'on a peer'}); "
                           "using the per-step NCCL loop")
-            if ok:
+            if set_up:
                 h.call("nufi_mg_teardown")
 
     def _run_exchange_steps(self, first: int, outputs: dict, ev) -> None:

@@ -112,3 +112,74 @@ def test_two_rank_exchange_bit_identical(name, steps):
     run = O.OracleRun(O.case(name)).run(steps)
     scale = np.abs(run["rho"]).max(axis=1, keepdims=True)
     assert (np.abs(ref - run["rho"]) / scale).max() < 1e-12
+
+
+# ---------------------------------------------------------------------------
+# the fused-exchange decision is collective (dist.DistributedSimulation._connect_fused)
+# ---------------------------------------------------------------------------
+
+class _FakeHandle:
+    """Stands in for the library handle: records the calls, fails nufi_mg_setup on request."""
+
+    def __init__(self, fail_setup, fail_connect=False):
+        self.fail_setup = fail_setup
+        self.fail_connect = fail_connect
+        self.calls = []
+
+        class _Lib:
+            @staticmethod
+            def nufi_mg_handle_size():
+                return 64
+
+        self.lib = _Lib()
+
+    def call(self, name, *args):
+        self.calls.append(name)
+        if name == "nufi_mg_setup" and self.fail_setup:
+            raise RuntimeError("setup failed on this rank")
+        if name == "nufi_mg_connect" and self.fail_connect:
+            raise RuntimeError("connect failed on this rank")
+
+
+def _agree_worker(rank, world, port, fail_rank, fail_what, q):
+    import types
+
+    from paper_2301_05581_b200.dist import DistributedSimulation
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        obj = DistributedSimulation.__new__(DistributedSimulation)
+        obj.torch, obj.dist, obj.group = torch, dist, None
+        obj.rank, obj.world = rank, world
+        h = _FakeHandle(fail_setup=(rank == fail_rank and fail_what == "setup"),
+                        fail_connect=(rank == fail_rank and fail_what == "connect"))
+        obj.history = types.SimpleNamespace(handle=h)
+        DistributedSimulation._connect_fused.__wrapped__(obj, 0)  # the undecorated body (no CUDA stream)
+        q.put((rank, obj.fused, h.calls))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank,fail_what", [(-1, None), (1, "setup"), (0, "connect")])
+def test_fused_exchange_decision_is_collective(fail_rank, fail_what):
+    """a rank whose peer-memory setup or connect fails must not leave its peers in
+    mismatched collectives -- every rank reaches the all_gather and the all_reduce, and all
+    ranks take the same decision (fused, or all fall back and tear down)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_agree_worker, args=(r, 2, port, fail_rank, fail_what, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r, (f, c)) for r, f, c in (q.get(timeout=120) for _ in procs))
+    for p in procs:
+        p.join(timeout=60)
+    fused = {r: v[0] for r, v in res.items()}
+    assert fused[0] == fused[1] == (fail_rank < 0)
+    for r, (_, calls) in res.items():
+        assert calls[0] == "nufi_mg_setup"
+        if fail_rank >= 0 and not (fail_what == "setup" and r == fail_rank):
+            # a rank whose own setup succeeded leaves multi-rank mode again
+            assert calls[-1] == "nufi_mg_teardown"
