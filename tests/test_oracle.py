@@ -157,3 +157,23 @@ def test_generic_trace_matches_reference_install_field(base):
     Xu, Vu = z["x"].copy(), z["v"].copy()
     O.trace_generic({k: ("uniform", z["E_uniform"]) for k in range(n + 1)}, c.L, n, c.tau, Xu, Vu, True)
     assert np.array_equal(Xu, z["X_uniform"]) and np.array_equal(Vu, z["V_uniform"])
+
+
+def test_wl3_full_size_golden_consistent():
+    """The full-size d = 3 fixture (16^3 x 32^3, generated by the unmodified reference for all
+    80 steps) against the oracle's Poisson / spline restatement on its own densities, the
+    evaluation counter and the background density (no trace: 134M points per step)."""
+    g = golden("wl3")
+    if g is None:
+        pytest.skip("golden not generated")
+    c = O.case("wl3")
+    N = len(g["W"]) - 1
+    keep = g["rho"].shape[0]
+    for n in range(0, keep, 5):
+        phi, hat = O.solve_poisson(c, g["rho"][n].reshape((c.Nx,) * 3))
+        coeffs = O.fit_spline(c, phi)
+        assert normwise(np.asarray(coeffs).reshape(1, -1), g["coeffs"][n:n + 1])[0] <= 1e-12
+        W = O.electric_energy(c, hat)
+        assert abs(W - g["W"][n]) <= 1e-12 * abs(g["W"][n])
+    assert int(g["field_evals"][-1]) == O.point_steps(c, N)
+    assert abs(O.background_density(c) - float(g["rho_bar"])) <= 1e-15
