@@ -253,56 +253,11 @@ __device__ __forceinline__ void dft_pass(const double *__restrict__ ire, const d
     __syncthreads();
 }
 
-// One separable radix-2 FFT pass along the axis of stride st (N = 2^logN): the same
-// transform as dft_pass -- out[.. alpha ..] = sum_x in[.. x ..] e^{sign 2 pi i alpha x / N}
-// -- in N log N: a bit-reversed copy along the axis into (ore, oim), then log2 N in-place
-// butterfly stages (decimation in time), a CTA barrier after each.
-__device__ __forceinline__ void fft_axis_pass(const double *__restrict__ ire, const double *__restrict__ iim,
-                                              double *__restrict__ ore, double *__restrict__ oim,
-                                              const double *__restrict__ twc, const double *__restrict__ tws,
-                                              int N, int logN, int nodes, int st, double sign) {
-    // N and st are powers of two here: every index split is a shift or a mask
-    const int T = blockDim.x;
-    const int logst = 31 - __clz(st);
-    for (int e = threadIdx.x; e < nodes; e += T) {
-        const int x = (e >> logst) & (N - 1);
-        const int rx = (int)(__brev((unsigned)x) >> (32 - logN));
-        const int dst = e + ((rx - x) << logst);
-        ore[dst] = ire[e];
-        oim[dst] = iim[e];
-    }
-    __syncthreads();
-    for (int lh = 0; lh < logN; ++lh) {
-        const int h = 1 << lh;
-        const int tws_shift = logN - 1 - lh;  // twiddle index pos * N / (2h)
-        const int loglines = 31 - __clz(nodes) - logN;  // lines = nodes / N
-        for (int b = threadIdx.x; b < (nodes >> 1); b += T) {
-            // consecutive lanes: along the line for the contiguous axis (st = 1), across
-            // lines otherwise -- either way neighbouring lanes touch neighbouring banks
-            const int line = st == 1 ? b >> (logN - 1) : b & ((1 << loglines) - 1);
-            const int j = st == 1 ? b & ((N >> 1) - 1) : b >> loglines;
-            const int pos = j & (h - 1);
-            const int i0 = ((j - pos) << 1) + pos;
-            const int base = ((line >> logst) << (logst + logN)) + (line & (st - 1));
-            const int a0 = base + (i0 << logst), a1 = a0 + (h << logst);
-            const double wr = twc[pos << tws_shift], wi = sign * tws[pos << tws_shift];
-            const double ur = ore[a1], ui = oim[a1];
-            const double xr = fma(ur, wr, -ui * wi), xi = fma(ur, wi, ui * wr);
-            const double pr = ore[a0], pi = oim[a0];
-            ore[a1] = pr - xr;
-            oim[a1] = pi - xi;
-            ore[a0] = pr + xr;
-            oim[a0] = pi + xi;
-        }
-        __syncthreads();
-    }
-}
-
 // One separable FFT along the axis of stride st = 2^logst (N = 2^logN), Stockham autosort
 // (no bit-reversal pass): one radix-2 stage when logN is odd, then radix-4 stages, each a
 // shared-memory ping-pong between (ar, ai) and (br, bi) with one CTA barrier -- log4 N + 1
-// passes over the data instead of log2 N + 1.  Same transform as fft_axis_pass:
-// out[.. alpha ..] = sum_x in[.. x ..] e^{sign 2 pi i alpha x / N}.  On return (ar, ai)
+// passes over the data instead of the log2 N + 1 of a radix-2 pass sequence with a
+// bit-reversal copy.  The transform: out[.. alpha ..] = sum_x in[.. x ..] e^{sign 2 pi i alpha x / N}.  On return (ar, ai)
 // hold the result (the pointers are swapped once per stage).
 __device__ __forceinline__ void fft_axis_stockham(double *&ar, double *&ai, double *&br, double *&bi,
                                                   const double *__restrict__ twc, const double *__restrict__ tws,
