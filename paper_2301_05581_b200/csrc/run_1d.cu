@@ -126,8 +126,9 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 3
     int fills = 0;
     unsigned gen = 0;
     // groups consumed so far by this CTA (uniform over its threads): the ring stage the next
-    // group lands in is gsum % stages
-    long long gsum = 0;
+    // group lands in is gs_mod (= groups so far mod stages, kept incrementally: a 64-bit modulo
+    // on the path from the barrier into the tail cost ~130 ns per step)
+    unsigned gs_mod = 0;
     const int my_tiles = lc < tiles_r ? (tiles_r - lc + nct - 1) / nct : 0;
     const size_t stage_doubles = (size_t)SPS * SLAB;
     bool pref_ready = false;  // this step's first group was issued before the previous tail
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 3
             __syncthreads();
         }
 
-        gsum += (long long)my_tiles * groups;
+        gs_mod = (gs_mod + (unsigned)(my_tiles * groups) % (unsigned)stages) % (unsigned)stages;
         pref_ready = P.prefetch && my_tiles > 0 && n < P.n_last && n >= 1;  // (groups_next > 0 iff n >= 1)
         // all partials of step n are written
         if (P.stamps && blockIdx.x == 0 && threadIdx.x == 0) P.stamps[3 * (n - P.n_first)] = globaltimer();
@@ -444,8 +445,8 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 3
         fp.ev_local = slabN;
         double *tail_ws = tail;
         if (pref_ready) {
-            // the next step's first group is landing in stage gsum % stages: work in the next one
-            tail_ws = ring + (size_t)((gsum + 1) % stages) * stage_doubles;
+            // the next step's first group is landing in stage gs_mod: work in the next one
+            tail_ws = ring + (size_t)(gs_mod + 1 == (unsigned)stages ? 0u : gs_mod + 1) * stage_doubles;
             fp.stage_cap = (int64_t)stage_doubles - field_smem_doubles(nodes, N, true);
         } else {
             fp.stage_cap = (int64_t)ring_doubles - field_smem_doubles(nodes, N, true);  // rest of the ring
