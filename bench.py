@@ -542,9 +542,12 @@ def gpu_arm(args, rank: int, world: int):
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(args.config)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak_nominal = sms * 64 * 2 * 1.965e9 / 1e12  # 64 DFMA / clk / SM at the 1965 MHz max clock
     roofline = {
         "bound": "fp64", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
         "frac": achieved / peak.value if peak.value else None,
+        "peak_nominal": peak_nominal, "frac_nominal": achieved / peak_nominal,
         "traffic": traffic["traffic"] if traffic else None,
         "traffic_detail": traffic,
         "kernel": ("run_1d_kernel (persistent: all steps, trace + grid barrier + field tail)" if g.d == 1
