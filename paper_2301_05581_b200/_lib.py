@@ -14,7 +14,10 @@ import os
 from .errors import ConfigError, NumericalConsistencyError, UsageError, VpflowError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libnufi_b200.so")
+# experiment builds of the same sources with other compile-time options live beside it
+# (make EXTRA=... LIB=../libnufi_b200_<tag>.so BUILD=build_<tag>); NUFI_LIB_VARIANT=<tag> loads one
+_VARIANT = os.environ.get("NUFI_LIB_VARIANT", "")
+LIB_PATH = os.path.join(HERE, f"libnufi_b200_{_VARIANT}.so" if _VARIANT else "libnufi_b200.so")
 
 NUFI_OK = 0
 NUFI_ERR_USAGE = 1

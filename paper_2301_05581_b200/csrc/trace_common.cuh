@@ -165,6 +165,30 @@ __device__ __forceinline__ void kick(const double (&X)[D], double (&V)[D], const
     }
 }
 
+// The d = 1 folded update from the located cell's coefficients (kick polynomial
+// q = A + B fc + C fc^2, pre-scaled): V <- V + q, X <- (X - V) - q.  Two rounding orders,
+// chosen by N alone so that every d = 1 path of one grid (run_1d, trace_rho_1d, trace_rho,
+// any rank split) computes the same bits:
+//  - N <= 64: few points per SM, the run is bound by the substep's dependent chain
+//    (profiles/r02_d1_chain_floor.txt).  X = ((X - V) - A - fc B) - fc^2 C puts the
+//    last-loaded coefficient C one DFMA from the next cell lookup (two in Horner form),
+//    for two more FP64 ops per substep;
+//  - N > 64: throughput-bound (FP64 pipe and shared-memory wavefronts), the 5-op Horner form.
+__host__ __device__ constexpr bool d1_wform(int N) { return N <= 64; }
+
+__device__ __forceinline__ void d1_fold(double &X, double &V, double fc, double A, double B, double C, bool wform) {
+    const double XmV = X - V;
+    if (wform) {
+        const double w = fc * fc;
+        X = fma(-w, C, fma(-fc, B, XmV - A));
+        V = fma(w, C, fma(fc, B, V + A));
+    } else {
+        const double t = fma(fc, C, B);
+        X = fma(-fc, t, XmV - A);
+        V = fma(fc, t, V + A);
+    }
+}
+
 // d = 1 substep with the drift folded into the kick (run_1d.cu kick1): on entry X is the
 // already drifted position of this substep, on exit the drifted position of the next one,
 // X - V_new = (X - V) - A - fc (B + fc C): the next cell lookup does not wait for a DADD.
@@ -175,10 +199,7 @@ __device__ __forceinline__ void kick1_folded(double &X, double &V, const double 
     const int i = locate_centred<POW2>(X, N, fc);
     double A, B, C;
     d1_fetch(slab, i, N, A, B, C);
-    const double XmV = X - V;
-    const double t = fma(fc, C, B);
-    X = fma(-fc, t, XmV - A);
-    V = fma(fc, t, V + A);
+    d1_fold(X, V, fc, A, B, C, d1_wform(N));
 }
 
 // shared-window alignment of the d = 1 slab rings: a multiple of 8 N for every N with a
@@ -201,16 +222,13 @@ __device__ __forceinline__ void kick1s(double &X, double &V, unsigned sbase) {
     static_assert(NX > 0 && (NX & (NX - 1)) == 0, "power-of-two N");
     const double s = X + MAGIC;
     const double fc = X - (s - MAGIC);
-    const double XmV = X - V;
     const unsigned lo = (unsigned)__double_as_longlong(s);
     const unsigned addr = ((lo << 3) & (unsigned)(8 * NX - 8)) | sbase;
-    double A, B, C;
+    double A, B, C;  // issued A, B, C: C (loaded last) is the one the W form consumes last
     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(A) : "r"(addr));
     asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(B) : "r"(addr), "n"(8 * NX));
     asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(C) : "r"(addr), "n"(16 * NX));
-    const double t = fma(fc, C, B);
-    X = fma(-fc, t, XmV - A);
-    V = fma(fc, t, V + A);
+    d1_fold(X, V, fc, A, B, C, d1_wform(NX));
 }
 
 // One backward substep: drift x -= tau v, then kick through slab.

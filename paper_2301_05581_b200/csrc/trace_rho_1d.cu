@@ -31,23 +31,14 @@ __device__ __forceinline__ void kick1d(double &X, double &V, const double *__res
     const double s = X + MAGIC;
     const int n_ = NX ? NX : N;
     const double fc = X - (s - MAGIC);
-    const double XmV = X - V;
     double A, B, C;
     d1_fetch(slab, (int)((unsigned)__double_as_longlong(s) & (unsigned)(n_ - 1)), n_, A, B, C);
-    const double t = fma(fc, C, B);
-    X = fma(-fc, t, XmV - A);
-    V = fma(fc, t, V + A);
+    d1_fold(X, V, fc, A, B, C, d1_wform(n_));
 }
 
+// runtime N (any value): the shared folded kick
 __device__ __forceinline__ void kick1d_any(double &X, double &V, const double *__restrict__ slab, int N) {
-    double fc;
-    const int i = locate_centred<false>(X, N, fc);
-    double A, B, C;
-    d1_fetch(slab, i, N, A, B, C);
-    const double t = fma(fc, C, B);
-    const double XmV = X - V;
-    X = fma(-fc, t, XmV - A);
-    V = fma(fc, t, V + A);
+    kick1_folded<false>(X, V, slab, N);
 }
 
 // NX: compile-time Nx (power of two) or 0 (runtime N, any value); SPS: slabs per stage.
