@@ -16,7 +16,7 @@ from .errors import ConfigError, NumericalConsistencyError, UsageError, VpflowEr
 HERE = os.path.dirname(os.path.abspath(__file__))
 # experiment builds of the same sources with other compile-time options live beside it
 # (make EXTRA=... LIB=../libnufi_b200_<tag>.so BUILD=build_<tag>); NUFI_LIB_VARIANT=<tag> loads one
-_VARIANT = os.environ.get("NUFI_LIB_VARIANT", "")
+_VARIANT = "".join(ch for ch in os.environ.get("NUFI_LIB_VARIANT", "") if ch.isalnum() or ch == "_")
 LIB_PATH = os.path.join(HERE, f"libnufi_b200_{_VARIANT}.so" if _VARIANT else "libnufi_b200.so")
 
 NUFI_OK = 0

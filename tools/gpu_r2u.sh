@@ -8,4 +8,4 @@ import json; d=json.loads(open("gpurun_out/u_${c}.log").read().strip().splitline
 print("$c", round(d["ms_per_step"],3), "frac", round(r["frac"],4), d["clocks"])
 PY
 done
-timeout 300 python tools/stamps.py ts1 2>/dev/null | head -3
+for c in ts1 wl1; do timeout 300 python tools/stamps.py $c 2>/dev/null | grep -v "^  n=" ; done
