@@ -44,7 +44,10 @@ class AsyncRing:
         self.next = (slot + 1) % SLOTS
         old = self.owner[slot]
         if old is not None:
-            old.materialize()
+            try:
+                old.materialize()
+            except Exception:  # noqa: BLE001 - kept in old._error, raised to its holder on read
+                pass
         self.owner[slot] = entry
         return slot
 
