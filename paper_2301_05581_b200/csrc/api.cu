@@ -967,10 +967,19 @@ static int refuse_installed(nufi_handle *h) {
     return NUFI_OK;
 }
 
+// the dense override table (4 doubles per step) covers `step`; a step far beyond anything the
+// history can hold is a usage error, not a host allocation that would throw through the C-ABI
+static int ovr_cover(nufi_handle *h, int64_t step) {
+    if (step < 0) return fail(NUFI_ERR_USAGE, "step index must be >= 0");
+    if (step >= std::max<int64_t>(h->cap, (int64_t)1 << 20))
+        return fail(NUFI_ERR_USAGE, "step index beyond the history's reach (max(capacity, 2^20))");
+    if ((size_t)(4 * (step + 1)) > h->ovr.size()) h->ovr.resize(4 * (size_t)(step + 1), 0.0);
+    return NUFI_OK;
+}
+
 int nufi_set_uniform_field(nufi_handle *h, int64_t step, const double *E0) {
     CHECK_HANDLE(h);
-    if (step < 0) return fail(NUFI_ERR_USAGE, "step index must be >= 0");
-    if ((size_t)(4 * (step + 1)) > h->ovr.size()) h->ovr.resize(4 * (size_t)(step + 1), 0.0);
+    if (int rc = ovr_cover(h, step)) return rc;
     const bool was = h->ovr[4 * step] != 0.0;
     h->ovr_spline.erase(step);
     if (E0) {
@@ -985,8 +994,7 @@ int nufi_set_uniform_field(nufi_handle *h, int64_t step, const double *E0) {
 
 int nufi_set_spline_field(nufi_handle *h, int64_t step, const double *coeffs) {
     CHECK_HANDLE(h);
-    if (step < 0) return fail(NUFI_ERR_USAGE, "step index must be >= 0");
-    if ((size_t)(4 * (step + 1)) > h->ovr.size()) h->ovr.resize(4 * (size_t)(step + 1), 0.0);
+    if (int rc = ovr_cover(h, step)) return rc;
     const bool was = h->ovr[4 * step] != 0.0;
     for (int a = 0; a < 4; ++a) h->ovr[4 * step + a] = 0.0;
     h->ovr_spline.erase(step);
@@ -1643,6 +1651,7 @@ int nufi_profiling_read(nufi_handle *h, double *out8) {
 
 int nufi_trace(nufi_handle *h, int64_t n, double *X, double *V, int64_t M, int half_kick, int mode, int64_t *evals) {
     CHECK_HANDLE(h);
+    if (M < 0) return fail(NUFI_ERR_USAGE, "point count must be >= 0");
     if (n < 0) return fail(NUFI_ERR_USAGE, "step index must be >= 0");
     if (mode != NUFI_TRACE_FAST && mode != NUFI_TRACE_PARITY) return fail(NUFI_ERR_USAGE, "unknown trace mode");
     if (n == 0) return NUFI_OK;  // kernels.py:397-398
@@ -1773,6 +1782,7 @@ int nufi_moments(nufi_handle *h, int64_t n, double *out, int64_t *evals) {
 
 int nufi_eval_field(nufi_handle *h, int64_t slot, const double *X, int64_t M, double *phi_out, double *E_out) {
     CHECK_HANDLE(h);
+    if (M < 0) return fail(NUFI_ERR_USAGE, "point count must be >= 0");
     if (slot < 0 || slot >= h->len) return fail(NUFI_ERR_USAGE, "history has no entry at that index");  // spline.py:144-146
     if (M == 0) return NUFI_OK;
     if (!X) return fail(NUFI_ERR_USAGE, "null points");
@@ -1854,6 +1864,7 @@ int nufi_inverse_transform(nufi_handle *h, const double *spec_re, const double *
 
 int nufi_bspline_weights(nufi_handle *h, const double *t, int64_t M, double *w_out, double *dw_out) {
     CHECK_HANDLE(h);
+    if (M < 0) return fail(NUFI_ERR_USAGE, "point count must be >= 0");
     if (M == 0) return NUFI_OK;
     if (!t || (!w_out && !dw_out)) return fail(NUFI_ERR_USAGE, "null argument");
     const size_t bytes = (size_t)M * sizeof(double);
@@ -1878,6 +1889,7 @@ int nufi_bspline_weights(nufi_handle *h, const double *t, int64_t M, double *w_o
 
 int nufi_eval_f0(nufi_handle *h, const double *X, const double *V, int64_t M, double *F) {
     CHECK_HANDLE(h);
+    if (M < 0) return fail(NUFI_ERR_USAGE, "point count must be >= 0");
     if (M == 0) return NUFI_OK;
     if (!X || !V || !F) return fail(NUFI_ERR_USAGE, "null argument");
     const size_t bytes = (size_t)M * h->d * sizeof(double);

@@ -161,3 +161,26 @@ def test_install_spline_field(base):
     with pytest.raises(vpflow.UsageError):
         density.compute_rho(ctx, n)  # the fused density kernel traces stored splines only
     ctx.install_field(0, None)
+
+
+def test_abi_rejects_negative_counts_and_unreachable_override_steps():
+    """C-ABI validation (include/nufi.h): a negative point count and an override step no
+    history can reach are usage errors, never a huge allocation."""
+    w = workload("kat_wl")
+    hist = spline.PotentialHistory(w.grid, w.tau, capacity=4)
+    flow.FlowContext(history=hist, ic=w.ic, tau=w.tau, grid=w.grid)
+    h = hist.handle
+    buf = np.zeros(64)
+    p = buf.ctypes.data
+    for fn, args in [("nufi_trace", (1, p, p, -1, 0, 0, None)),
+                     ("nufi_eval_f0", (p, p, -1, p)),
+                     ("nufi_bspline_weights", (p, -1, p, p))]:
+        with pytest.raises(vpflow.UsageError):
+            h.call(fn, *args)
+    for fn in ("nufi_set_uniform_field", "nufi_set_spline_field"):
+        with pytest.raises(vpflow.UsageError):
+            h.call(fn, 1 << 40, p)
+        with pytest.raises(vpflow.UsageError):
+            h.call(fn, -1, p)
+    h.call("nufi_set_uniform_field", 2, p)  # a step beyond the stored history is fine
+    h.call("nufi_set_uniform_field", 2, None)
