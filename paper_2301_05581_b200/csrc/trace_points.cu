@@ -232,6 +232,8 @@ __global__ void __launch_bounds__(256, 2)
     const double s_in = tau * inv_h, s_out = 1.0 / s_in, hx = 1.0 / inv_h;
     const int64_t per_pass = (int64_t)32 * warps * PPT;
     int it = 0;
+    int s = 0;         // ring stage of iteration it and its fill parity, kept incrementally
+    uint32_t ph = 0u;  // (no integer division per stage; trace_rho.cu)
     for (int pass = 0; pass < passes; ++pass) {
         const int64_t base = ((int64_t)blockIdx.x * passes + pass) * per_pass + (int64_t)warp * PPT * 32 + lane;
         double Xs[PPT][D], Vs[PPT][D];
@@ -247,10 +249,8 @@ __global__ void __launch_bounds__(256, 2)
             if (half_kick) kick<D, POW2, NX>(Xs[pp], Vs[pp], ev_hist + (size_t)n * slab_elems, N, K, true);
         }
         for (int st = 0; st < stages_per_pass; ++st, ++it) {
-            const int s = it % stages;
-            const uint32_t u = (uint32_t)(it / stages);
             const int k_hi = n - 1 - st * sps, k_lo = max(0, k_hi - sps + 1);
-            mbar_wait(&full[s], u & 1u);
+            mbar_wait(&full[s], ph);
             const double *buf = ring + (size_t)s * sps * slab_elems;
             for (int k = k_hi; k >= k_lo; --k) {
                 const double *slab = buf + (size_t)(k - k_lo) * slab_elems;
@@ -270,6 +270,7 @@ __global__ void __launch_bounds__(256, 2)
                     }
                 }
             }
+            if (++s == stages) s = 0, ph ^= 1u;
         }
 #pragma unroll
         for (int pp = 0; pp < PPT; ++pp) {

@@ -175,6 +175,8 @@ __global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams 
 #pragma unroll
     for (int q = 0; q < NS; ++q) mom[q] = 0.0;
     int it = 0;
+    int s = 0;         // ring stage of iteration it (= it % stages), kept incrementally:
+    uint32_t ph = 0u;  // and its fill parity ((it / stages) & 1) -- no integer division per stage
     for (int pass = 0; pass < p.passes; ++pass) {
         double X[PPT][D], V[PPT][D];
         int64_t jrow[PPT];
@@ -197,11 +199,9 @@ __global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams 
         }
 
         for (int st = 0; st < stages_per_pass; ++st, ++it) {
-            const int s = it % stages;
-            const uint32_t u = (uint32_t)(it / stages);
             const int k_hi = n - 1 - st * sps;
             const int k_lo = max(0, k_hi - sps + 1);
-            if (!GL) mbar_wait(&full[s], u & 1u);
+            if (!GL) mbar_wait(&full[s], ph);
             const double *buf = GL ? p.ev_hist + (size_t)k_lo * slab_elems : ring + (size_t)s * sps * slab_elems;
             // slab 0 is stored pre-halved (field_common.cuh), so every kick is uniform
             if constexpr (D == 1) {
@@ -241,6 +241,7 @@ __global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams 
                     }
                 }
             }
+            if (++s == stages) s = 0, ph ^= 1u;
         }
 
 #pragma unroll
