@@ -205,13 +205,40 @@ __global__ void field_tables_kernel(double *tw, double *fac, double *k2t, int d,
 // (coefficients, spline.py:78-84 o poisson.py:105-110) and
 // gp[m] = sum_alpha fac[alpha] sym[alpha] cos(2 pi alpha m / N) (nodal potential,
 // poisson.py:85-87); fac already carries the 1/N of the inverse transform.
-__global__ void field_conv_kernels_kernel(const double *fac, double *gc, double *gp, int N) {
+// (grids too large for the staged tables below: the same values, formed per tap)
+__global__ void field_conv_kernels_direct(const double *fac, double *gc, double *gp, int N) {
     for (int m = threadIdx.x + blockIdx.x * blockDim.x; m < N; m += blockDim.x * gridDim.x) {
         double a = 0.0, b = 0.0;
         for (int al = 0; al < N; ++al) {
-            const double cs = cospi(2.0 * (double)((al * m) % N) / (double)N);
+            const double cs = cospi(2.0 * (double)(((int64_t)al * m) % N) / (double)N);
             a = fma(fac[al], cs, a);
             b = fma(fac[al] * fac[N + al], cs, b);
+        }
+        gc[m] = a;
+        gp[m] = b;
+    }
+}
+
+__global__ void field_conv_kernels_kernel(const double *fac, double *gc, double *gp, int N) {
+    // the N distinct cosines, fac and fac * sym staged once (the values and the summation
+    // order of the direct form: one cospi per (alpha, m) and an integer modulo per tap
+    // made this ~28 us per handle); (alpha m) mod N advanced incrementally
+    extern __shared__ double tab[];
+    double *cs = tab, *f1 = tab + N, *f2 = tab + 2 * N;
+    for (int j = threadIdx.x; j < N; j += blockDim.x) {
+        cs[j] = cospi(2.0 * (double)j / (double)N);
+        f1[j] = fac[j];
+        f2[j] = fac[j] * fac[N + j];
+    }
+    __syncthreads();
+    for (int m = threadIdx.x + blockIdx.x * blockDim.x; m < N; m += blockDim.x * gridDim.x) {
+        double a = 0.0, b = 0.0;
+        int idx = 0;  // (al * m) % N
+        for (int al = 0; al < N; ++al) {
+            a = fma(f1[al], cs[idx], a);
+            b = fma(f2[al], cs[idx], b);
+            idx += m;
+            if (idx >= N) idx -= N;
         }
         gc[m] = a;
         gp[m] = b;
@@ -224,7 +251,16 @@ cudaError_t launch_field_tables(double *tw, double *fac, double *k2, int d, int 
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || d != 1) return e;
     // d = 1: gc, gp follow k2 in the table buffer
-    field_conv_kernels_kernel<<<1, 256, 0, st>>>(fac, k2 + nodes, k2 + nodes + N, N);
+    const size_t smem = 3 * (size_t)N * sizeof(double);
+    if (smem > 200 * 1024) {
+        field_conv_kernels_direct<<<(N + 255) / 256, 256, 0, st>>>(fac, k2 + nodes, k2 + nodes + N, N);
+        return cudaGetLastError();
+    }
+    if (smem > 48 * 1024) {
+        e = cudaFuncSetAttribute(field_conv_kernels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    field_conv_kernels_kernel<<<1, 256, smem, st>>>(fac, k2 + nodes, k2 + nodes + N, N);
     return cudaGetLastError();
 }
 
