@@ -863,11 +863,8 @@ static __device__ __forceinline__ bool field_update_1d_body(const FieldParams &p
         // the stored (and traced) slab; E at the nodes comes from the fit itself
         const double c0 = hist_round(e0, p.f32_hist), c1 = hist_round(e1, p.f32_hist),
                      c2 = hist_round(e2, p.f32_hist), c3 = hist_round(e3, p.f32_hist);
-        const double g0 = 0.5 * (c2 - c0);
-        const double g1 = (c0 - 2.0 * c1) + c2;
-        const double g2 = (1.5 * (c1 - c2)) + 0.5 * (c3 - c0);
-        const double K = evs * p.K;
-        const double A = K * ((g0 + 0.5 * g1) + 0.25 * g2), Bc = K * (g1 + g2), C = K * g2;
+        double A, Bc, C;
+        d1_cell_poly(c0, c1, c2, c3, evs * p.K, A, Bc, C);
         if (evg) {
             evg[d1_ia(i, N)] = A;
             evg[d1_ib(i, N)] = Bc;
@@ -1139,13 +1136,11 @@ static __device__ __forceinline__ bool field_update_body(const FieldParams &p, d
         for (int i = threadIdx.x; i < N; i += T) {
             const double c0 = hist_round(c[(i - 1 + N) % N], p.f32_hist), c1 = hist_round(c[i], p.f32_hist),
                          c2 = hist_round(c[(i + 1) % N], p.f32_hist), c3 = hist_round(c[(i + 2) % N], p.f32_hist);
-            const double g0 = 0.5 * (c2 - c0);
-            const double g1 = (c0 - 2.0 * c1) + c2;
-            const double g2 = (1.5 * (c1 - c2)) + 0.5 * (c3 - c0);
-            const double K = evs * p.K;
-            put(d1_ia(i, N), K * ((g0 + 0.5 * g1) + 0.25 * g2));
-            put(d1_ib(i, N), K * (g1 + g2));
-            put(d1_ic(i, N), K * g2);
+            double A, Bc, C;
+            d1_cell_poly(c0, c1, c2, c3, evs * p.K, A, Bc, C);
+            put(d1_ia(i, N), A);
+            put(d1_ib(i, N), Bc);
+            put(d1_ic(i, N), C);
         }
     } else {
         const int raw = ev_slab_raw_elems(d, N);

@@ -192,13 +192,11 @@ __global__ void large_append_kernel(LargeParams P, const double *c) {
                 const int i = (int)ii;
                 const double c0 = hist_round(c[(i - 1 + N) % N], p.f32_hist), c1 = hist_round(c[i], p.f32_hist),
                              c2 = hist_round(c[(i + 1) % N], p.f32_hist), c3 = hist_round(c[(i + 2) % N], p.f32_hist);
-                const double g0 = 0.5 * (c2 - c0);
-                const double g1 = (c0 - 2.0 * c1) + c2;
-                const double g2 = (1.5 * (c1 - c2)) + 0.5 * (c3 - c0);
-                const double K = evs * p.K;
-                evg[d1_ia(i, N)] = K * ((g0 + 0.5 * g1) + 0.25 * g2);
-                evg[d1_ib(i, N)] = K * (g1 + g2);
-                evg[d1_ic(i, N)] = K * g2;
+                double A, Bc, C;
+                d1_cell_poly(c0, c1, c2, c3, evs * p.K, A, Bc, C);
+                evg[d1_ia(i, N)] = A;
+                evg[d1_ib(i, N)] = Bc;
+                evg[d1_ic(i, N)] = C;
             }
         } else {
             const int raw = ev_slab_raw_elems(d, N);

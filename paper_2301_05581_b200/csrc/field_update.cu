@@ -292,12 +292,11 @@ __global__ void build_ev_slabs_kernel(double *__restrict__ hist, double *__restr
         K *= evs;
         for (int i = threadIdx.x; i < N; i += blockDim.x) {
             const double c0 = c[(i - 1 + N) % N], c1 = c[i], c2 = c[(i + 1) % N], c3 = c[(i + 2) % N];
-            const double g0 = 0.5 * (c2 - c0);
-            const double g1 = (c0 - 2.0 * c1) + c2;
-            const double g2 = (1.5 * (c1 - c2)) + 0.5 * (c3 - c0);
-            ev[d1_ia(i, N)] = K * ((g0 + 0.5 * g1) + 0.25 * g2);
-            ev[d1_ib(i, N)] = K * (g1 + g2);
-            ev[d1_ic(i, N)] = K * g2;
+            double A, Bc, C;
+            d1_cell_poly(c0, c1, c2, c3, K, A, Bc, C);
+            ev[d1_ia(i, N)] = A;
+            ev[d1_ib(i, N)] = Bc;
+            ev[d1_ic(i, N)] = C;
         }
     } else {
         const int raw = ev_slab_raw_elems(d, N);

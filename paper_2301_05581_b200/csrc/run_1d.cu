@@ -35,15 +35,15 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // One substep with the drift folded into the kick: on entry X is the already
 // drifted position of this substep; on exit X is the drifted position of the
 // next one, X - V_new = (X - V) - A - fc * (B + fc C), so the next cell lookup
-// does not wait for a separate drift DADD.  (Same arithmetic as trace_common.cuh
-// up to rounding order.)
+// does not wait for a separate drift DADD.  X is the shifted d = 1 state (d1_locate);
+// lookup and arithmetic are kick1s' (bit-identical).
 template <int NX>
 __device__ __forceinline__ void kick1(double &X, double &V, const double *__restrict__ slab, int N) {
-    const double s = X + MAGIC;
     const int n_ = NX ? NX : N;
-    const double fc = X - (s - MAGIC);
+    double fc;
+    const int i = d1_cell<true>(d1_locate(X, fc), n_);
     double A, B, C;
-    d1_fetch(slab, (int)((unsigned)__double_as_longlong(s) & (unsigned)(n_ - 1)), n_, A, B, C);
+    d1_fetch(slab, i, n_, A, B, C);
     d1_fold(X, V, fc, A, B, C, d1_wform(n_));
 }
 
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 3
                 const int j = d1_row(vt, warp, p.vt_per_block, p.B);
                 const double v0 = __dadd_rn(-p.vmax, __dmul_rn((double)j + 0.5, p.hv));  // grids.py:110-115
                 double V = v0 * p.vel_to_scaled;
-                double X = ((double)(valid ? node : 0) - 0.5) - V;  // first drift (folded form)
+                double X = ((double)(valid ? node : 0) - D1_OFF) - V;  // shifted state (d1_locate), first drift folded
                 if (n >= 1) {
                     if (NX)
                         kick1<NX>(X, V, slabN, N);
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 3
                     x = __dmul_rn((double)node, p.hx);  // grids.py:104-108
                     v = v0;
                 } else {
-                    x = ((X + V) + 0.5) * p.hx;  // undo the look-ahead drift of the last kick
+                    x = ((X + V) + D1_OFF) * p.hx;  // undo the look-ahead drift of the last kick
                     v = V * p.scaled_to_vel;
                 }
                 const double f = eval_f0<1>(p.f0, &x, &v);

@@ -9,14 +9,18 @@
 //     X = x * N/L - 1/2  (cell units, centred),   V = v * tau * N/L  (cells/step)
 // so a drift is one DADD and the cell lookup is the magic-constant rint of X:
 // cell i = rint(X) mod N, centred fraction fc = X - rint(X) in [-1/2, 1/2], and
-// the reference's fraction is f = fc + 1/2.  The kick scale
+// the reference's fraction is f = fc + 1/2.  d = 1 shifts the state instead:
+//     Y = x * N/L - 1/16,  s8 = Y + 1.5 * 2^49 (ulp 1/8)
+// leaves round(8 Y) in the low word of s8, whose bits >= 3 are 8 * floor(x N/L): the cell's
+// byte offset in a plane of doubles, OR-able into an aligned slab address with no shift on
+// the substep's dependent chain; the local coordinate is u = Y - cell = f - 1/16 (d1_locate).  The kick scale
 //     K = -tau^2 (N/L)^2    (V += K * dphi/dt-sum, i.e. tau*N/L * tau*E)
 // is folded into the evaluation slabs (d = 1) or applied once (d = 2, 3).
 //
 // Evaluation-slab layouts (written by field_update.cu, one per stored step):
 //   d = 1: three arrays [A | B | C] of N doubles: on cell i the kick is the
-//          quadratic A_i + fc*(B_i + fc*C_i)  (the B-spline derivative restricted
-//          to one cell, pre-multiplied by K);
+//          quadratic A_i + u*(B_i + u*C_i) in u = f - 1/16 (the B-spline derivative
+//          restricted to one cell, pre-multiplied by K; d1_cell_poly);
 //   d = 2: [R][R], d = 3: [R][R][R] with R = N + 3: raw coefficients with a
 //          periodic halo on every axis (halo index j' holds c[(j' - 1) mod N]),
 //          so the 4^d stencil of the cell with lower corner i is the block at
@@ -86,6 +90,41 @@ __device__ __forceinline__ void d1_fetch(const double *__restrict__ slab, int i,
     C = slab[2 * N + i];
 }
 
+// The kick polynomial of one d = 1 cell from the four spline coefficients c_{i-1} .. c_{i+2}:
+// -(d/dt) of the cubic B-spline sum on the cell is g0 + g1 f + g2 f^2 in the reference's
+// fraction f (kernels.py:164-182); stored in u = f - 1/16, pre-multiplied by the kick scale K.
+__host__ __device__ __forceinline__ void d1_cell_poly(double c0, double c1, double c2, double c3, double K,
+                                                      double &A, double &B, double &C) {
+    const double g0 = 0.5 * (c2 - c0);
+    const double g1 = (c0 - 2.0 * c1) + c2;
+    const double g2 = (1.5 * (c1 - c2)) + 0.5 * (c3 - c0);
+    A = K * ((g0 + 0.0625 * g1) + 0.00390625 * g2);
+    B = K * (g1 + 0.125 * g2);
+    C = K * g2;
+}
+
+// d = 1 state offset: Y = x * N/L - D1_OFF
+constexpr double D1_OFF = 0.0625;
+constexpr double MAGIC8 = 844424930131968.0;  // 1.5 * 2^49: ulp 1/8
+
+// d = 1 cell lookup on the shifted state Y: returns the low word of s8 = Y + MAGIC8, i.e.
+// round(8 Y) mod 2^32, whose bits >= 3 hold the cell floor(round(8 Y) / 8) = floor(x N/L)
+// (a tie of round(8 Y) only occurs on a cell boundary, where both neighbouring pieces agree);
+// u = Y - cell in [-1/16, 15/16) is the local coordinate of the stored polynomial.
+__device__ __forceinline__ unsigned d1_locate(double Y, double &u) {
+    const long long b = __double_as_longlong(Y + MAGIC8);
+    u = Y - (__longlong_as_double(b & ~7ll) - MAGIC8);
+    return (unsigned)b;
+}
+
+// cell index mod N from d1_locate's word (POW2: mask; else floor division and wrap)
+template <bool POW2>
+__device__ __forceinline__ int d1_cell(unsigned lo8, int N) {
+    if (POW2) return (int)(lo8 >> 3) & (N - 1);
+    const int i = ((int)lo8 >> 3) % N;
+    return i < 0 ? i + N : i;
+}
+
 template <bool POW2>
 __device__ __forceinline__ int wrap_idx(int i, int N) {
     if (POW2) return i & (N - 1);
@@ -99,9 +138,9 @@ template <int D, bool POW2, int NX = 0>
 __device__ __forceinline__ void kick(const double (&X)[D], double (&V)[D], const double *__restrict__ slab, int N_,
                                      double K, bool half) {
     const int N = NX ? NX : N_;  // compile-time N makes every stencil offset an immediate
-    if constexpr (D == 1) {
+    if constexpr (D == 1) {  // X[0] is the shifted state Y (d1_locate)
         double fc;
-        const int i = locate_centred<POW2>(X[0], N, fc);
+        const int i = d1_cell<POW2>(d1_locate(X[0], fc), N);
         double A, B, C;
         d1_fetch(slab, i, N, A, B, C);
         const double kick = fma(fc, fma(fc, C, B), A);
@@ -196,7 +235,7 @@ template <bool POW2, int NX = 0>
 __device__ __forceinline__ void kick1_folded(double &X, double &V, const double *__restrict__ slab, int N_) {
     const int N = NX ? NX : N_;
     double fc;
-    const int i = locate_centred<POW2>(X, N, fc);
+    const int i = d1_cell<POW2>(d1_locate(X, fc), N);
     double A, B, C;
     d1_fetch(slab, i, N, A, B, C);
     d1_fold(X, V, fc, A, B, C, d1_wform(N));
@@ -215,15 +254,14 @@ __device__ __forceinline__ double *d1_ring_base(unsigned char *smem) {
 
 // kick1 with the cell address formed by ONE 3-input LOP3: the slab's shared-window address
 // sbase is a multiple of N*8 (the ring is aligned to D1_RING_ALIGN bytes and every slab / stage
-// offset is a multiple of N*8), so base + 8*(i mod N) == ((8*i) & (8N-8)) | sbase -- the
-// add of the generic form (SHF, LOP3, IADD on the substep's dependent chain) disappears.
+// offset is a multiple of N*8), and d1_locate's word already holds 8 * cell in its bits >= 3,
+// so base + 8*(i mod N) == (word & (8N-8)) | sbase: DADD -> LOP3 -> LDS on the substep's
+// dependent chain (the centred rint form needed a shift and an add as well).
 template <int NX>
 __device__ __forceinline__ void kick1s(double &X, double &V, unsigned sbase) {
     static_assert(NX > 0 && (NX & (NX - 1)) == 0, "power-of-two N");
-    const double s = X + MAGIC;
-    const double fc = X - (s - MAGIC);
-    const unsigned lo = (unsigned)__double_as_longlong(s);
-    const unsigned addr = ((lo << 3) & (unsigned)(8 * NX - 8)) | sbase;
+    double fc;
+    const unsigned addr = (d1_locate(X, fc) & (unsigned)(8 * NX - 8)) | sbase;
     double A, B, C;  // issued A, B, C: C (loaded last) is the one the W form consumes last
     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(A) : "r"(addr));
     asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(B) : "r"(addr), "n"(8 * NX));

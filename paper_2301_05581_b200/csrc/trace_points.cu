@@ -180,7 +180,7 @@ __global__ void trace_points_fast(const double *__restrict__ ev_hist, int ev_sla
     double Xs[D], Vs[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-        Xs[a] = fma(X[p * D + a], inv_h, -0.5);
+        Xs[a] = fma(X[p * D + a], inv_h, D == 1 ? -D1_OFF : -0.5);
         Vs[a] = V[p * D + a] * s_in;
     }
     if (half_kick && n > 0) kick<D, POW2>(Xs, Vs, ev_hist + (size_t)n * ev_slab_elems, N, K, true);
@@ -189,7 +189,7 @@ __global__ void trace_points_fast(const double *__restrict__ ev_hist, int ev_sla
     for (int k = n - 1; k >= 0; --k) substep<D, POW2>(Xs, Vs, ev_hist + (size_t)k * ev_slab_elems, N, K, false);
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-        X[p * D + a] = (Xs[a] + 0.5) * hx;
+        X[p * D + a] = (Xs[a] + (D == 1 ? D1_OFF : 0.5)) * hx;
         V[p * D + a] = Vs[a] * s_out;
     }
 }
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(256, 2)
             const int64_t qq = q < M ? q : M - 1;  // the tail CTA's spare lanes trace a copy, never stored
 #pragma unroll
             for (int a = 0; a < D; ++a) {
-                Xs[pp][a] = fma(X[qq * D + a], inv_h, -0.5);
+                Xs[pp][a] = fma(X[qq * D + a], inv_h, D == 1 ? -D1_OFF : -0.5);
                 Vs[pp][a] = V[qq * D + a] * s_in;
             }
             if (half_kick) kick<D, POW2, NX>(Xs[pp], Vs[pp], ev_hist + (size_t)n * slab_elems, N, K, true);
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(256, 2)
             if (q < M)
 #pragma unroll
                 for (int a = 0; a < D; ++a) {
-                    X[q * D + a] = (Xs[pp][a] + 0.5) * hx;
+                    X[q * D + a] = (Xs[pp][a] + (D == 1 ? D1_OFF : 0.5)) * hx;
                     V[q * D + a] = Vs[pp][a] * s_out;
                 }
         }

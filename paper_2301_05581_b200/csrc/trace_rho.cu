@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams 
                 r /= p.Nv;
                 // grids.py:110-115: -vmax + (j + 0.5) * hv
                 const double v = __dadd_rn(-p.vmax, __dmul_rn((double)ja + 0.5, p.hv));
-                X[pp][a] = (double)ni[a] - 0.5;
+                X[pp][a] = (double)ni[a] - (D == 1 ? D1_OFF : 0.5);  // d = 1: shifted state (d1_locate)
                 V[pp][a] = v * p.vel_to_scaled;
             }
             // Psi's leading half kick through the step's own field (slab n, read in place)
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(256, 2) trace_rho_kernel(const TraceRhoParams 
             } else {
 #pragma unroll
                 for (int a = 0; a < D; ++a) {
-                    x[a] = (X[pp][a] + 0.5) * p.hx;
+                    x[a] = (X[pp][a] + (D == 1 ? D1_OFF : 0.5)) * p.hx;
                     v[a] = V[pp][a] * p.scaled_to_vel;
                 }
             }

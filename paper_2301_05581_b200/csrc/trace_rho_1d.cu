@@ -28,11 +28,11 @@ namespace nufi {
 // of this substep, on exit the drifted position of the next one.
 template <int NX>
 __device__ __forceinline__ void kick1d(double &X, double &V, const double *__restrict__ slab, int N) {
-    const double s = X + MAGIC;
     const int n_ = NX ? NX : N;
-    const double fc = X - (s - MAGIC);
+    double fc;
+    const int i = d1_cell<true>(d1_locate(X, fc), n_);
     double A, B, C;
-    d1_fetch(slab, (int)((unsigned)__double_as_longlong(s) & (unsigned)(n_ - 1)), n_, A, B, C);
+    d1_fetch(slab, i, n_, A, B, C);
     d1_fold(X, V, fc, A, B, C, d1_wform(n_));
 }
 
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(544) trace_rho_1d_kernel(const TraceRhoParams 
         const int j = d1_row(vt, warp, p.vt_per_block, p.B);
         const double v0 = __dadd_rn(-p.vmax, __dmul_rn((double)j + 0.5, p.hv));
         double V = v0 * p.vel_to_scaled;
-        double X = ((double)(valid ? node : 0) - 0.5) - V;  // first drift (folded form)
+        double X = ((double)(valid ? node : 0) - D1_OFF) - V;  // shifted state (d1_locate), first drift folded
         int s = 0;
         uint32_t ph = 0;
         const int top_cnt = n - (groups - 1) * SPS;  // slabs in the (partial) top group
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(544) trace_rho_1d_kernel(const TraceRhoParams 
             x = __dmul_rn((double)node, p.hx);
             v = v0;
         } else {
-            x = ((X + V) + 0.5) * p.hx;  // undo the look-ahead drift of the last kick
+            x = ((X + V) + D1_OFF) * p.hx;  // undo the look-ahead drift of the last kick
             v = V * p.scaled_to_vel;
         }
         const double f = eval_f0<1>(p.f0, &x, &v);
