@@ -32,26 +32,6 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-// One substep with the drift folded into the kick: on entry X is the already
-// drifted position of this substep; on exit X is the drifted position of the
-// next one, X - V_new = (X - V) - A - fc * (B + fc C), so the next cell lookup
-// does not wait for a separate drift DADD.  X is the shifted d = 1 state (d1_locate);
-// lookup and arithmetic are kick1s' (bit-identical).
-template <int NX>
-__device__ __forceinline__ void kick1(double &X, double &V, const double *__restrict__ slab, int N) {
-    const int n_ = NX ? NX : N;
-    double fc;
-    const int i = d1_cell<true>(d1_locate(X, fc), n_);
-    double A, B, C;
-    d1_fetch(slab, i, n_, A, B, C);
-    d1_fold(X, V, fc, A, B, C, d1_wform(n_));
-}
-
-// runtime N (any value): the shared folded kick
-__device__ __forceinline__ void kick1_any(double &X, double &V, const double *__restrict__ slab, int N) {
-    kick1_folded<false>(X, V, slab, N);
-}
-
 // doubles of the ring / tail-workspace union (16-byte aligned end for the barriers)
 __host__ __device__ inline size_t run_1d_ring_doubles(int stages, int sps, int slab, int nodes, int N) {
     const size_t ring = (size_t)stages * sps * slab, tail = (size_t)field_smem_doubles(nodes, N, true);
@@ -174,9 +154,9 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 3
                 double X = ((double)(valid ? node : 0) - D1_OFF) - V;  // shifted state (d1_locate), first drift folded
                 if (n >= 1) {
                     if (NX)
-                        kick1<NX>(X, V, slabN, N);
+                        kick1_folded<true, NX>(X, V, slabN, N);
                     else
-                        kick1_any(X, V, slabN, N);
+                        kick1_folded<false>(X, V, slabN, N);
                 }
                 long long wait_cyc = 0, t_start = clock64();
                 for (int it = 0; it < groups; ++it) {
@@ -192,9 +172,9 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 3
                         const int cnt = it == 0 ? top_cnt : SPS;
                         for (int q = cnt - 1; q >= 0; --q) {
                             if (NX)
-                                kick1<NX>(X, V, buf + q * SLAB, N);
+                                kick1_folded<true, NX>(X, V, buf + q * SLAB, N);
                             else
-                                kick1_any(X, V, buf + q * SLAB, N);
+                                kick1_folded<false>(X, V, buf + q * SLAB, N);
                         }
                     }
                     __syncwarp();

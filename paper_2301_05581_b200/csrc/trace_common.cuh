@@ -228,7 +228,8 @@ __device__ __forceinline__ void d1_fold(double &X, double &V, double fc, double 
     }
 }
 
-// d = 1 substep with the drift folded into the kick (run_1d.cu kick1): on entry X is the
+// d = 1 substep with the drift folded into the kick (every d = 1 path outside the shared-memory
+// ring fast path kick1s, which has the same lookup and arithmetic): on entry X is the
 // already drifted position of this substep, on exit the drifted position of the next one,
 // X - V_new = (X - V) - A - fc (B + fc C): the next cell lookup does not wait for a DADD.
 template <bool POW2, int NX = 0>

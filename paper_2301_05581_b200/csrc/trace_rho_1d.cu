@@ -23,24 +23,6 @@
 
 namespace nufi {
 
-// Folded-drift kick, identical arithmetic to run_1d.cu's kick1 (so compute_rho,
-// nufi_step and nufi_run agree bit for bit): on entry X is the drifted position
-// of this substep, on exit the drifted position of the next one.
-template <int NX>
-__device__ __forceinline__ void kick1d(double &X, double &V, const double *__restrict__ slab, int N) {
-    const int n_ = NX ? NX : N;
-    double fc;
-    const int i = d1_cell<true>(d1_locate(X, fc), n_);
-    double A, B, C;
-    d1_fetch(slab, i, n_, A, B, C);
-    d1_fold(X, V, fc, A, B, C, d1_wform(n_));
-}
-
-// runtime N (any value): the shared folded kick
-__device__ __forceinline__ void kick1d_any(double &X, double &V, const double *__restrict__ slab, int N) {
-    kick1_folded<false>(X, V, slab, N);
-}
-
 // NX: compile-time Nx (power of two) or 0 (runtime N, any value); SPS: slabs per stage.
 // Block = C consumer warps (one point per thread) + 1 producer warp that keeps
 // the TMA ring full, so no consumer ever waits for a refill it did not need.
@@ -111,9 +93,9 @@ __global__ void __launch_bounds__(544) trace_rho_1d_kernel(const TraceRhoParams 
                 const int cnt = it == 0 ? top_cnt : SPS;
                 for (int q = cnt - 1; q >= 0; --q) {
                     if (NX != 0)
-                        kick1d<NX>(X, V, buf + q * SLAB, N);
+                        kick1_folded<true, NX>(X, V, buf + q * SLAB, N);
                     else
-                        kick1d_any(X, V, buf + q * SLAB, N);
+                        kick1_folded<false>(X, V, buf + q * SLAB, N);
                 }
             }
             __syncwarp();
