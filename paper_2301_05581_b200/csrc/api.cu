@@ -269,6 +269,41 @@ static void pinned_put(double *p, size_t elems) {
     pinned_cache().free_blocks.push_back({elems, p});
 }
 
+// Library-owned streams are recycled across handles (creating + destroying a stream costs
+// ~90 us of host time, a third of a small run's end-to-end overhead); a stream returns to
+// the pool idle (nufi_destroy synchronises it first).  Bounded per device.
+struct StreamPool {
+    std::mutex mu;
+    std::map<int, std::vector<cudaStream_t>> free_streams;
+};
+static StreamPool &stream_pool() {
+    static StreamPool *p = new StreamPool();  // never destroyed: no teardown-order issues
+    return *p;
+}
+static cudaError_t stream_get(int device, cudaStream_t *st) {
+    {
+        std::lock_guard<std::mutex> lk(stream_pool().mu);
+        auto &v = stream_pool().free_streams[device];
+        if (!v.empty()) {
+            *st = v.back();
+            v.pop_back();
+            return cudaSuccess;
+        }
+    }
+    return cudaStreamCreateWithFlags(st, cudaStreamNonBlocking);
+}
+static void stream_put(int device, cudaStream_t st) {
+    {
+        std::lock_guard<std::mutex> lk(stream_pool().mu);
+        auto &v = stream_pool().free_streams[device];
+        if (v.size() < 16) {
+            v.push_back(st);
+            return;
+        }
+    }
+    cudaStreamDestroy(st);
+}
+
 static int ipow(int b, int e) {
     int r = 1;
     for (int i = 0; i < e; ++i) r *= b;
@@ -519,7 +554,7 @@ int nufi_create(const nufi_config *cfg, int device, void *stream, nufi_handle **
     if (stream) {
         h->stream = (cudaStream_t)stream;
     } else {
-        CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        CU(stream_get(device, &h->stream));
         h->own_stream = true;
     }
     const nufi_config &c = *cfg;
@@ -540,11 +575,13 @@ int nufi_create(const nufi_config *cfg, int device, void *stream, nufi_handle **
     // v-blocks (fixed combine order, independent of the rank count)
     int B = c.v_blocks > 0 ? c.v_blocks : 8;
     if (B > 8) {
+        if (h->own_stream) stream_put(device, h->stream);
         delete h;
         return fail(NUFI_ERR_USAGE, "v_blocks must be <= 8");
     }
     while (B > 1 && (h->V % B != 0)) --B;
     if (c.v_blocks > 0 && B != c.v_blocks) {
+        if (h->own_stream) stream_put(device, h->stream);
         delete h;
         return fail(NUFI_ERR_USAGE, "v_blocks must divide Nv^d");
     }
@@ -552,6 +589,7 @@ int nufi_create(const nufi_config *cfg, int device, void *stream, nufi_handle **
     h->b_lo = c.block_hi > c.block_lo ? c.block_lo : 0;
     h->b_hi = c.block_hi > c.block_lo ? c.block_hi : B;
     if (h->b_lo < 0 || h->b_hi > B) {
+        if (h->own_stream) stream_put(device, h->stream);
         delete h;
         return fail(NUFI_ERR_USAGE, "block range outside [0, v_blocks)");
     }
@@ -652,7 +690,7 @@ int nufi_destroy(nufi_handle *h) {
     }
     cudaStreamSynchronize(h->stream);  // frees complete -> the pool can hand the memory to the next handle
     pinned_put(h->run_host, h->run_elems);
-    if (h->own_stream) cudaStreamDestroy(h->stream);
+    if (h->own_stream) stream_put(h->device, h->stream);  // idle: synchronised above
     delete h;
     return NUFI_OK;
 }

@@ -24,3 +24,19 @@ for it in range(7):
     t5 = time.perf_counter()
     if it >= 2:
         print(f"cfg {1e6*(t1-t0):.0f} us  nufi_create {1e6*(t2-t1):.0f} us  sync {1e6*(t3-t2):.0f} us  set_ic {1e6*(t4-t3):.0f} us  destroy {1e6*(t5-t4):.0f} us", flush=True)
+# the same with a caller stream (no stream create / destroy inside the library)
+s = torch.cuda.Stream()
+for it in range(7):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    cfg = _lib.make_config(w.grid, _placeholder_ic(w.grid), w.tau, w.n_steps, rho_bar=1.0)
+    t1 = time.perf_counter()
+    h = ctypes.c_void_p()
+    lib.nufi_create(ctypes.byref(cfg), 0, ctypes.c_void_p(s.cuda_stream), ctypes.byref(h))
+    t2 = time.perf_counter()
+    lib.nufi_sync(h)
+    t3 = time.perf_counter()
+    lib.nufi_destroy(h)
+    t5 = time.perf_counter()
+    if it >= 2:
+        print(f"caller stream: nufi_create {1e6*(t2-t1):.0f} us  sync {1e6*(t3-t2):.0f} us  destroy {1e6*(t5-t3):.0f} us", flush=True)
