@@ -57,7 +57,8 @@ struct FieldParams {
     double *ev_local;   // optional second destination of the evaluation slab (persistent kernel smem)
     int *status;        // NUFI_ERR_NUMERICAL when rho is not neutral
     int *status_mirror; // optional (e.g. pinned host): *status copied here when the tail ends
-    int64_t *hist_len;  // device-side history length (slot + 1)
+    int64_t *hist_len;  // device-side history length: slot + 1 after the append, slot after a failed
+                        // neutrality check (what nufi_check_status reconciles the host length to)
     int finish_only;    // compute_rho only: stop after rho / stats
     int f32_hist;       // FP32 history (spline.py:118-125): stored slabs rounded to float
     unsigned long long *tstamps;  // debug: phase timestamps (thread 0), 10 slots
@@ -815,6 +816,7 @@ static __device__ __forceinline__ bool field_update_1d_body(const FieldParams &p
             const bool bad = fabs(s2 * (1.0 / (double)N)) > 1e-8 * m;
             scratch[96] = bad ? 1.0 : 0.0;
             if (bad && p.status) *p.status = NUFI_ERR_NUMERICAL;
+            if (bad && p.hist_len) *p.hist_len = p.slot;  // the device length: this slot not appended
         }
     }
     // sampled f min / max (the per-warp partials of phase A) in another warp, off warp 0's path
@@ -1061,6 +1063,7 @@ static __device__ __forceinline__ bool field_update_body(const FieldParams &p, d
         const double tol = 1e-8 * m;
         if (fabs(mean) > tol) {
             if (threadIdx.x == 0 && p.status) *p.status = NUFI_ERR_NUMERICAL;
+            if (threadIdx.x == 0 && p.hist_len) *p.hist_len = p.slot;  // this slot not appended
             return false;  // history unchanged (the reference raises before appending)
         }
     }

@@ -112,7 +112,10 @@ __global__ void large_check_kernel(LargeParams P, int ctas) {
             s += P.part[c];
             m = fmax(m, P.part[ctas + c]);
         }
-        if (fabs(s / (double)p.nodes) > 1e-8 * m && p.status) *p.status = NUFI_ERR_NUMERICAL;
+        if (fabs(s / (double)p.nodes) > 1e-8 * m) {
+            if (p.status) *p.status = NUFI_ERR_NUMERICAL;
+            if (p.hist_len) *p.hist_len = p.slot;  // the device length: this slot not appended
+        }
     }
 }
 

@@ -79,3 +79,28 @@ def test_device_density_replaced_falls_back_to_host_values():
             nufi.compute_rho(ctx, n)  # a second density replaces the device copy
         u = nufi.advance(ctx, r.density)
         assert abs(u.W - ref.W[n]) <= 1e-13 * abs(ref.W[n])
+
+
+def test_device_side_failure_reconciles_the_length_after_truncate():
+    """A tail that fails its neutrality check on the device reports the history length as
+    its own slot (nothing appended), so the host length is reconciled correctly even when
+    the device's previous length is stale (a truncate, or an uncommitted speculative step)."""
+    from paper_2301_05581_b200.pending import Entry, ring_of
+
+    w = workload("kat_wl")
+    sim = nufi.Simulation(w.grid, w.ic, w.tau, 10)
+    sim.run()
+    hist = sim.history
+    assert len(hist) == 11
+    hist.truncate(5)
+    r = nufi.compute_rho(sim.ctx, 5)  # speculative whole step 5 (uncommitted)
+    _ = r.density.values
+    ring = ring_of(hist)
+    e = Entry(ring, "field")
+    bad = np.ones(w.grid.n_nodes)  # not neutral: the device check fails (the host check is bypassed)
+    hist.handle.call("nufi_field_update_async", bad.ctypes.data, e.slot)
+    with pytest.raises(nufi.NumericalConsistencyError):
+        e.materialize()
+    assert len(hist) == 5
+    u = nufi.advance(sim.ctx, nufi.compute_rho(sim.ctx, 5).density)  # the loop carries on
+    assert len(hist) == 6 and u.W > 0
