@@ -189,7 +189,7 @@ __device__ __forceinline__ void grid_barrier(unsigned *counter, unsigned target)
         unsigned v;
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
         while (v < target) {
-            __nanosleep(NUFI_BARRIER_SLEEP_NS);
+            if (NUFI_BARRIER_SLEEP_NS > 0) __nanosleep(NUFI_BARRIER_SLEEP_NS);
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
         }
     }
@@ -205,7 +205,7 @@ __device__ __forceinline__ void grid_barrier_wd(unsigned *counter, unsigned targ
         unsigned v;
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
         while (v < target && *(volatile const int *)err == 0) {
-            __nanosleep(NUFI_BARRIER_SLEEP_NS);
+            if (NUFI_BARRIER_SLEEP_NS > 0) __nanosleep(NUFI_BARRIER_SLEEP_NS);
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
         }
     }

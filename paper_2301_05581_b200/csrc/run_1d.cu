@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 3
                             atomicExch(P.mg_error, 1);
                             break;
                         }
-                        __nanosleep(NUFI_BARRIER_SLEEP_NS);
+                        if (NUFI_BARRIER_SLEEP_NS > 0) __nanosleep(NUFI_BARRIER_SLEEP_NS);
                     }
                 }
             }
