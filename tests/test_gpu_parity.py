@@ -242,3 +242,29 @@ def test_baseline_config_vs_reference(name):
         assert res.W[t > 30].min() > 0.1 and res.W.max() < 1.0
     else:
         _check_run(name, g, sim, res)
+
+
+@pytest.mark.parametrize("hk", [0, 1])
+def test_trace_fast_d1_cell_boundaries_and_rounding_ties(hk):
+    """The d = 1 FAST lookup rounds 8 Y (Y = x N/L - 1/16, csrc/trace_common.cuh d1_locate);
+    its ties fall exactly on cell boundaries.  Points on every node (boundaries), 1/16 and
+    1/2 cell either side, and outside [0, L), with v = 0 (so the first lookups hit those
+    positions exactly) and small v: FAST within 1e-11 of the reference's arithmetic (PARITY)."""
+    t = golden("trace_kat_wl")
+    if t is None:
+        pytest.skip("trace golden missing")
+    n = int(t["n"])
+    w, h = _hist_from("kat_wl", t["coeffs"], n + 1)
+    g = w.grid
+    hx = g.L / g.Nx
+    k = np.arange(-2, g.Nx + 3, dtype=np.float64)
+    x = np.concatenate([k, k + 1 / 16, k - 1 / 16, k + 0.5, k + 15 / 16]) * hx
+    v = np.concatenate([np.zeros_like(x), np.full_like(x, 1e-3), np.full_like(x, -0.37)])
+    X0 = np.tile(x, 3)[:, None].copy()
+    V0 = v[:, None].copy()
+    Xp, Vp = X0.copy(), V0.copy()
+    nufi.trace_backward(h, n, Xp, Vp, bool(hk), nufi.TRACE_PARITY)
+    Xf, Vf = X0.copy(), V0.copy()
+    nufi.trace_backward(h, n, Xf, Vf, bool(hk), nufi.TRACE_FAST)
+    assert np.abs(Xf - Xp).max() <= 1e-11 * max(1.0, np.abs(Xp).max())
+    assert np.abs(Vf - Vp).max() <= 1e-11 * max(1.0, np.abs(Vp).max())
