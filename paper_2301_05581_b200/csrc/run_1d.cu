@@ -115,15 +115,27 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 3
 
         const bool pref_now = pref_ready;
         pref_ready = false;
-        for (int t_loc = lc; t_loc < tiles_r; t_loc += nct) {
-            const int tile = tile_lo + t_loc;
+        // PAIR (the WIDE, many-tiles-per-CTA kernel): two tiles per pass share one stream of
+        // the history through the ring (half the ring-fill traffic into shared memory, which
+        // the gathers of this shared-memory-bound kernel compete with) and give every thread
+        // two independent chains.  Each point's arithmetic and each tile's fixed-order CTA
+        // v-sum are unchanged, so the results are bit-identical to one tile per pass.
+        constexpr bool PAIR = WIDE != 0;
+        for (int t_loc = lc; t_loc < tiles_r; t_loc += (PAIR ? 2 : 1) * nct) {
             const bool first_tile = t_loc == lc;
+            const bool hasB = PAIR && t_loc + nct < tiles_r;
             static constexpr bool kAlt = false;  // tile mapping: v-tile-major (true) or node-tile-major
             const int vts = P.tiles / p.node_tiles;
-            const int nt = kAlt ? tile / vts : tile % p.node_tiles;
-            const int vt = kAlt ? tile % vts : tile / p.node_tiles;
-            const int node = nt * 32 + lane;
-            double acc = 0.0, fmn = DBL_MAX, fmx = -DBL_MAX;
+            int nt2[2], vt2[2], node2[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int tile = tile_lo + t_loc + (u ? nct : 0);
+                nt2[u] = kAlt ? tile / vts : tile % p.node_tiles;
+                vt2[u] = kAlt ? tile % vts : tile / p.node_tiles;
+                node2[u] = nt2[u] * 32 + lane;
+            }
+            double f2[2] = {0.0, 0.0};
+            bool valid2[2] = {false, false};
             if (producer) {
                 const int it0 = (pref_now && first_tile) ? 1 : 0;  // group 0 already in flight
                 if (lane == 0) {
@@ -147,16 +159,25 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 3
                     }
                 }
             } else if (warp < cw) {
-                const bool valid = node < nodes;
-                const int j = d1_row(vt, warp, p.vt_per_block, p.B);
-                const double v0 = __dadd_rn(-p.vmax, __dmul_rn((double)j + 0.5, p.hv));  // grids.py:110-115
-                double V = v0 * p.vel_to_scaled;
-                double X = ((double)(valid ? node : 0) - D1_OFF) - V;  // shifted state (d1_locate), first drift folded
+                double X2[2], V2[2], v02[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    valid2[u] = node2[u] < nodes && (u == 0 || hasB);
+                    const int j = d1_row(vt2[u], warp, p.vt_per_block, p.B);
+                    v02[u] = __dadd_rn(-p.vmax, __dmul_rn((double)j + 0.5, p.hv));  // grids.py:110-115
+                    V2[u] = v02[u] * p.vel_to_scaled;
+                    // shifted state (d1_locate), first drift folded
+                    X2[u] = ((double)(node2[u] < nodes ? node2[u] : 0) - D1_OFF) - V2[u];
+                }
                 if (n >= 1) {
-                    if (NX)
-                        kick1_folded<true, NX>(X, V, slabN, N);
-                    else
-                        kick1_folded<false>(X, V, slabN, N);
+#pragma unroll
+                    for (int u = 0; u < (PAIR ? 2 : 1); ++u) {
+                        if (u == 1 && !hasB) break;
+                        if (NX)
+                            kick1_folded<true, NX>(X2[u], V2[u], slabN, N);
+                        else
+                            kick1_folded<false>(X2[u], V2[u], slabN, N);
+                    }
                 }
                 long long wait_cyc = 0, t_start = clock64();
                 for (int it = 0; it < groups; ++it) {
@@ -166,15 +187,27 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 3
                     const double *buf = ring + (size_t)s_ring * SPS * SLAB;
                     if (NX != 0 && (it > 0 || top_cnt == SPS)) {
                         const unsigned b32 = (unsigned)__cvta_generic_to_shared(buf);
+                        if (PAIR && hasB) {
 #pragma unroll
-                        for (int q = SPS - 1; q >= 0; --q) kick1s<NX ? NX : 64>(X, V, b32 + q * SLAB * 8);
+                            for (int q = SPS - 1; q >= 0; --q) {
+                                kick1s<NX ? NX : 64>(X2[0], V2[0], b32 + q * SLAB * 8);
+                                kick1s<NX ? NX : 64>(X2[1], V2[1], b32 + q * SLAB * 8);
+                            }
+                        } else {
+#pragma unroll
+                            for (int q = SPS - 1; q >= 0; --q) kick1s<NX ? NX : 64>(X2[0], V2[0], b32 + q * SLAB * 8);
+                        }
                     } else {
                         const int cnt = it == 0 ? top_cnt : SPS;
                         for (int q = cnt - 1; q >= 0; --q) {
-                            if (NX)
-                                kick1_folded<true, NX>(X, V, buf + q * SLAB, N);
-                            else
-                                kick1_folded<false>(X, V, buf + q * SLAB, N);
+#pragma unroll
+                            for (int u = 0; u < (PAIR ? 2 : 1); ++u) {
+                                if (u == 1 && !hasB) break;
+                                if (NX)
+                                    kick1_folded<true, NX>(X2[u], V2[u], buf + q * SLAB, N);
+                                else
+                                    kick1_folded<false>(X2[u], V2[u], buf + q * SLAB, N);
+                            }
                         }
                     }
                     __syncwarp();
@@ -187,50 +220,62 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 3
                     P.stamps[o] = (unsigned long long)wait_cyc;
                     P.stamps[o + 1] = (unsigned long long)(clock64() - t_start);
                 }
-                double x, v;
-                if (n == 0) {
-                    x = __dmul_rn((double)node, p.hx);  // grids.py:104-108
-                    v = v0;
-                } else {
-                    x = ((X + V) + D1_OFF) * p.hx;  // undo the look-ahead drift of the last kick
-                    v = V * p.scaled_to_vel;
-                }
-                const double f = eval_f0<1>(p.f0, &x, &v);
-                if (valid) acc = fmn = fmx = f;
-                red[threadIdx.x] = acc;
-                red[32 * cw + threadIdx.x] = fmn;
-                red[64 * cw + threadIdx.x] = fmx;
-            }
-            __syncthreads();
-            // fixed-order CTA v-sum in warp 0 (on the critical path to the barrier), the sampled
-            // (min, max) in another warp alongside
-            const int mmw = cw > 1 ? 1 : 0;
-            if (warp == 0) {
-                double sum = 0.0;
-                for (int w = 0; w < cw; ++w) sum += red[w * 32 + lane];
-                if (node < nodes) part[(size_t)vt * nodes + node] = sum;
-            }
-            if (warp == mmw) {
-                double mn = DBL_MAX, mx = -DBL_MAX;
-                for (int w = 0; w < cw; ++w) {
-                    mn = fmin(mn, red[32 * cw + w * 32 + lane]);
-                    mx = fmax(mx, red[64 * cw + w * 32 + lane]);
-                }
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-                    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-                }
-                if (lane == 0) {
-                    const size_t c = (size_t)vt * p.node_tiles + nt;
-                    fmm[2 * c] = mn;
-                    fmm[2 * c + 1] = mx;
+                for (int u = 0; u < (PAIR ? 2 : 1); ++u) {
+                    double x, v;
+                    if (n == 0) {
+                        x = __dmul_rn((double)node2[u], p.hx);  // grids.py:104-108
+                        v = v02[u];
+                    } else {
+                        x = ((X2[u] + V2[u]) + D1_OFF) * p.hx;  // undo the look-ahead drift of the last kick
+                        v = V2[u] * p.scaled_to_vel;
+                    }
+                    f2[u] = eval_f0<1>(p.f0, &x, &v);
                 }
             }
-            __syncthreads();
+            // per tile: the fixed-order CTA v-sum in warp 0 (on the critical path to the
+            // barrier), the sampled (min, max) in another warp alongside
+            const int mmw = cw > 1 ? 1 : 0;
+#pragma unroll
+            for (int u = 0; u < (PAIR ? 2 : 1); ++u) {
+                if (u == 1 && !hasB) break;
+                if (warp < cw) {
+                    const double acc = valid2[u] ? f2[u] : 0.0;
+                    red[threadIdx.x] = acc;
+                    red[32 * cw + threadIdx.x] = valid2[u] ? f2[u] : DBL_MAX;
+                    red[64 * cw + threadIdx.x] = valid2[u] ? f2[u] : -DBL_MAX;
+                }
+                __syncthreads();
+                if (warp == 0) {
+                    double sum = 0.0;
+                    for (int w = 0; w < cw; ++w) sum += red[w * 32 + lane];
+                    if (node2[u] < nodes) part[(size_t)vt2[u] * nodes + node2[u]] = sum;
+                }
+                if (warp == mmw) {
+                    double mn = DBL_MAX, mx = -DBL_MAX;
+                    for (int w = 0; w < cw; ++w) {
+                        mn = fmin(mn, red[32 * cw + w * 32 + lane]);
+                        mx = fmax(mx, red[64 * cw + w * 32 + lane]);
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                    }
+                    if (lane == 0) {
+                        const size_t c = (size_t)vt2[u] * p.node_tiles + nt2[u];
+                        fmm[2 * c] = mn;
+                        fmm[2 * c + 1] = mx;
+                    }
+                }
+                __syncthreads();
+            }
         }
 
-        gs_mod = (gs_mod + (unsigned)(my_tiles * groups) % (unsigned)stages) % (unsigned)stages;
+        {
+            const int my_passes = WIDE ? (my_tiles + 1) / 2 : my_tiles;  // ring streams this step
+            gs_mod = (gs_mod + (unsigned)(my_passes * groups) % (unsigned)stages) % (unsigned)stages;
+        }
         pref_ready = P.prefetch && my_tiles > 0 && n < P.n_last && n >= 1;  // (groups_next > 0 iff n >= 1)
         // all partials of step n are written
         if (P.stamps && blockIdx.x == 0 && threadIdx.x == 0) P.stamps[3 * (n - P.n_first)] = globaltimer();
