@@ -223,6 +223,10 @@ int nufi_rho_async(nufi_handle *h, int64_t n, int slot, int64_t *evals, int *spe
 int nufi_commit_async(nufi_handle *h, int64_t n);
 int nufi_field_update_async(nufi_handle *h, const double *rho, int slot);
 int nufi_async_wait(nufi_handle *h, int slot, double **entry);
+/* The ring as one contiguous pinned block: *base = entry 0, entry q at *base + q * *slot_elems
+ * (a host binding can map it once instead of per entry; an entry is complete once its event
+ * -- or the handle's stream (nufi_sync) -- has been waited for). */
+int nufi_async_ring(nufi_handle *h, double **base, int64_t *slot_elems);
 
 /* One full step n (requires len == n): nufi_rho + nufi_field_update, all on
  * the device.  Outputs optional. */

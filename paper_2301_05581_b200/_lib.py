@@ -107,6 +107,7 @@ _SIGS = {
     "nufi_commit_async": [_P, _I64],
     "nufi_field_update_async": [_P, _P, ctypes.c_int],
     "nufi_async_wait": [_P, ctypes.c_int, ctypes.POINTER(ctypes.POINTER(ctypes.c_double))],
+    "nufi_async_ring": [_P, ctypes.POINTER(ctypes.POINTER(ctypes.c_double)), ctypes.POINTER(ctypes.c_int64)],
     "nufi_step": [_P, _I64, _P, _P, _P, _P, _I64P],
     "nufi_run": [_P, _I64, _P, _P, _P, _P, _I64P],
     "nufi_trace": [_P, _I64, _P, _P, _I64, ctypes.c_int, ctypes.c_int, _I64P],

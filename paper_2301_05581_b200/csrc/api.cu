@@ -165,7 +165,9 @@ struct nufi_handle {
 
     // stream-ordered drop-in calls (nufi_rho_async / nufi_field_update_async): a ring of
     // pinned host entries [rho | stats 3 | W 1 | pad | E nodes*d | coeffs nodes], one event each
-    std::vector<double *> aring;
+    std::vector<double *> aring;     // per-slot pointers into aring_block
+    double *aring_block = nullptr;   // one contiguous pinned block of all slots
+    size_t aring_block_elems = 0;
     std::vector<cudaEvent_t> aev;
     size_t aslot_elems = 0;
     bool d_rho_async = false;  // d_rho holds the density of the last nufi_rho_async
@@ -684,10 +686,8 @@ int nufi_destroy(nufi_handle *h) {
                     (void *)h->large_scratch, (void *)h->halo, (void *)h->tile_cnt, (void *)h->block_mm})
         if (p) cudaFreeAsync(p, h->stream);
     mg_release(h);
-    for (size_t q = 0; q < h->aring.size(); ++q) {
-        pinned_put(h->aring[q], h->aslot_elems);
-        cudaEventDestroy(h->aev[q]);
-    }
+    for (size_t q = 0; q < h->aev.size(); ++q) cudaEventDestroy(h->aev[q]);
+    pinned_put(h->aring_block, h->aring_block_elems);
     cudaStreamSynchronize(h->stream);  // frees complete -> the pool can hand the memory to the next handle
     pinned_put(h->run_host, h->run_elems);
     if (h->own_stream) stream_put(h->device, h->stream);  // idle: synchronised above
@@ -1142,17 +1142,26 @@ int nufi_async_slots(nufi_handle *h, int slots) {
     CHECK_HANDLE(h);
     if (slots < 1 || slots > 4096) return fail(NUFI_ERR_USAGE, "slots must be 1..4096");
     CU(cudaStreamSynchronize(h->stream));
-    for (size_t q = 0; q < h->aring.size(); ++q) {
-        pinned_put(h->aring[q], h->aslot_elems);
-        cudaEventDestroy(h->aev[q]);
-    }
+    for (size_t q = 0; q < h->aev.size(); ++q) cudaEventDestroy(h->aev[q]);
+    pinned_put(h->aring_block, h->aring_block_elems);
+    h->aring_block = nullptr;
     h->aring.assign(slots, nullptr);
     h->aev.assign(slots, nullptr);
     h->aslot_elems = (size_t)h->nodes * (2 + h->d) + 6;
+    h->aring_block_elems = (size_t)slots * h->aslot_elems;
+    CU(pinned_get(&h->aring_block, h->aring_block_elems));
     for (int q = 0; q < slots; ++q) {
-        CU(pinned_get(&h->aring[q], h->aslot_elems));
+        h->aring[q] = h->aring_block + (size_t)q * h->aslot_elems;
         CU(cudaEventCreateWithFlags(&h->aev[q], cudaEventDisableTiming));
     }
+    return NUFI_OK;
+}
+
+int nufi_async_ring(nufi_handle *h, double **base, int64_t *slot_elems) {
+    CHECK_HANDLE(h);
+    if (!base || !slot_elems) return fail(NUFI_ERR_USAGE, "null argument");
+    *base = h->aring_block;
+    *slot_elems = (int64_t)h->aslot_elems;
     return NUFI_OK;
 }
 
@@ -1246,6 +1255,8 @@ int nufi_async_wait(nufi_handle *h, int slot, double **entry) {
     if (st != 0) {
         int rc = nufi_check_status(h);  // reconciles len, clears the flag, sets the message
         if (rc) return rc;
+        // the failure was reported through an earlier entry: this entry's work was skipped
+        return fail(st, "step skipped: an earlier enqueued step failed (density not neutral)");
     }
     if (entry) *entry = h->aring[slot];
     return NUFI_OK;

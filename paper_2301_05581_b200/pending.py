@@ -16,7 +16,11 @@ committing it -- so advance() of that (unmodified) density only commits the slot
 (modified values, another step, a user array) takes the separate tail launch.
 
 A ring slot is reused every SLOTS calls; before that the result object still holding it
-is materialised (it copies its values out), so results stay valid indefinitely.
+is materialised (it copies its values out, waiting only for that entry), so results stay
+valid indefinitely.  The ring is one contiguous pinned block mapped once (nufi_async_ring).
+A read by the caller waits for everything enqueued so far (one stream wait), and any wait
+marks every older entry complete (the stream is in order), so reading a loop's results
+after it costs one wait, not one per entry.
 """
 
 from __future__ import annotations
@@ -29,23 +33,31 @@ SLOTS = 64
 
 
 class AsyncRing:
-    """The per-history ring of pinned result entries (nufi_async_slots)."""
+    """The per-history ring of pinned result entries (nufi_async_slots / nufi_async_ring)."""
 
     def __init__(self, history):
         self.history = history
         self.handle = history.handle
-        self.handle.call("nufi_async_slots", SLOTS)
-        self.owner = [None] * SLOTS
+        self.nodes = history.grid.n_nodes
+        self.slots = SLOTS
+        self.handle.call("nufi_async_slots", self.slots)
+        base = ctypes.POINTER(ctypes.c_double)()
+        stride = ctypes.c_int64(0)
+        self.handle.call("nufi_async_ring", ctypes.byref(base), ctypes.byref(stride))
+        self.view = np.ctypeslib.as_array(base, shape=(self.slots, stride.value))  # mapped once
+        self.owner = [None] * self.slots
         self.next = 0
+        self.seq = 0  # entries created so far
+        self.synced = 0  # every entry with seq <= synced is complete on the device
         self.last_rho = None  # the entry whose density is still on the device (d_rho)
 
     def acquire(self, entry) -> int:
         slot = self.next
-        self.next = (slot + 1) % SLOTS
+        self.next = (slot + 1) % self.slots
         old = self.owner[slot]
         if old is not None:
             try:
-                old.materialize()
+                old.materialize(own=True)  # wait for that entry only: no drain of newer work
             except Exception:  # noqa: BLE001 - kept in old._error, raised to its holder on read
                 pass
         self.owner[slot] = entry
@@ -55,12 +67,14 @@ class AsyncRing:
 class Entry:
     """One enqueued call's outputs, read from its pinned ring entry on first access."""
 
-    __slots__ = ("ring", "slot", "kind", "n", "_data", "_error")
+    __slots__ = ("ring", "slot", "kind", "n", "seq", "_data", "_error")
 
     def __init__(self, ring: AsyncRing, kind: str, n: int = -1):
         self.ring = ring
         self.kind = kind  # "rho" (rho, stats), "field" (W, E, coeffs) or "step" (all five)
         self.n = n
+        ring.seq += 1
+        self.seq = ring.seq
         self.slot = ring.acquire(self)
         self._data = None
         self._error = None
@@ -70,24 +84,36 @@ class Entry:
         if self.ring.owner[self.slot] is self:
             self.ring.owner[self.slot] = None
 
-    def materialize(self) -> dict:
+    def materialize(self, own: bool = False) -> dict:
+        """The entry's values (copied out of the ring).  own=False (a caller's read): wait for
+        everything enqueued so far, one stream wait; own=True (the slot is about to be
+        reused): wait for this entry's event only."""
         if self._data is not None:
             return self._data
         if self._error is not None:
             raise self._error
         ring = self.ring
-        ptr = ctypes.POINTER(ctypes.c_double)()
+        nodes = ring.nodes
         try:
-            ring.handle.call("nufi_async_wait", self.slot, ctypes.byref(ptr))
-        except Exception as exc:  # a failed tail (non-neutral density) surfaces here
+            if self.seq > ring.synced:
+                if own:
+                    ring.handle.call("nufi_async_wait", self.slot, None)
+                    ring.synced = max(ring.synced, self.seq)  # in-order stream: older ones too
+                else:
+                    ring.handle.call("nufi_sync")
+                    ring.synced = ring.seq
+            if ring.view[self.slot, nodes + 4:nodes + 5].view(np.int32)[0] != 0:
+                ring.handle.call("nufi_async_wait", self.slot, None)  # reconciles and raises
+        except Exception as exc:  # a failed (or skipped) tail surfaces here
             self._error = exc
             if ring.owner[self.slot] is self:
                 ring.owner[self.slot] = None
             raise
+        row = ring.view[self.slot]
         g = ring.history.grid
-        nodes, d = g.n_nodes, g.d
+        d = g.d
         # one copy of the whole entry out of the pinned ring; the fields are views of it
-        flat = np.ctypeslib.as_array(ptr, shape=(nodes * (2 + d) + 6,)).copy()
+        flat = row.copy()
         data = {}
         if self.kind in ("rho", "step"):
             data["rho"] = flat[:nodes].reshape(g.shape_x)

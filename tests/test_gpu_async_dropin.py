@@ -104,3 +104,28 @@ def test_device_side_failure_reconciles_the_length_after_truncate():
     assert len(hist) == 5
     u = nufi.advance(sim.ctx, nufi.compute_rho(sim.ctx, 5).density)  # the loop carries on
     assert len(hist) == 6 and u.W > 0
+
+
+def test_entries_after_a_device_failure_raise_too():
+    """Steps enqueued after one whose tail failed are skipped on the device; reading any of
+    them raises (not stale values), also after the first failure was reported."""
+    from paper_2301_05581_b200.pending import Entry, ring_of
+
+    w = workload("kat_wl")
+    hist = nufi.PotentialHistory(w.grid, w.tau, capacity=16)
+    ctx = nufi.FlowContext(history=hist, ic=w.ic, tau=w.tau, grid=w.grid)
+    for n in range(3):
+        nufi.advance(ctx, nufi.compute_rho(ctx, n).density)
+    ring = ring_of(hist)
+    bad = np.ones(w.grid.n_nodes)  # not neutral: the device check fails (host check bypassed)
+    e1 = Entry(ring, "field")
+    hist.handle.call("nufi_field_update_async", bad.ctypes.data, e1.slot)
+    good = nufi.compute_rho(ctx, 3)  # enqueued behind the failure: skipped on the device
+    u2 = nufi.advance(ctx, good.density)
+    with pytest.raises(nufi.NumericalConsistencyError):
+        e1.materialize()
+    with pytest.raises(nufi.NumericalConsistencyError):
+        _ = u2.W
+    assert len(hist) == 3
+    u = nufi.advance(ctx, nufi.compute_rho(ctx, 3).density)  # the loop recovers
+    assert len(hist) == 4 and u.W > 0
