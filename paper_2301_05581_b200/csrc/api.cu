@@ -136,6 +136,7 @@ struct nufi_handle {
     double *hist = nullptr, *ev_hist = nullptr;
     double *partial = nullptr, *fminmax = nullptr, *blocks = nullptr;
     double *d_rho = nullptr, *d_E = nullptr, *d_W = nullptr, *d_stats = nullptr, *d_rho_bar = nullptr;
+    double *row_last = nullptr;  // split d = 1 runs: the helpers' last rows (+ (min, max) pairs), lazily
     double *tables = nullptr;  // field_common.cuh constant tables: 4N + 3 Nx^d doubles
     unsigned *ticket = nullptr;  // last-CTA-done counter of the fused d = 1 step
     unsigned *tile_cnt = nullptr;  // d >= 2 fused block reduce: node_tiles + 1 arrival counters
@@ -680,6 +681,7 @@ int nufi_destroy(nufi_handle *h) {
     cudaSetDevice(h->device);
     cudaStreamSynchronize(h->stream);
     for (void *p : {(void *)h->hist, (void *)h->ev_hist, (void *)h->partial, (void *)h->fminmax, (void *)h->blocks,
+                    (void *)h->row_last,
                     (void *)h->d_rho, (void *)h->d_E, (void *)h->d_W, (void *)h->d_stats, (void *)h->d_rho_bar,
                     (void *)h->d_status, (void *)h->d_len, (void *)h->run_dev, (void *)h->tables,
                     (void *)h->ticket, (void *)h->barrier, (void *)h->mom_part, (void *)h->d_mom,
@@ -1566,6 +1568,22 @@ int nufi_run(nufi_handle *h, int64_t n_last, double *rho_hist, double *E_hist, d
         P.prefetch = h->stages >= 2 &&
                      (int64_t)h->sps * h->ev_elems >= (int64_t)field_smem_doubles(h->nodes, h->N, true) &&
                      !getenv("NUFI_NOPREFETCH");
+        // split: with one tile per CTA and SMs to spare, helper CTAs trace every tile's last row
+        // so no SM holds more than vt_rows - 1 tracing warps (shared-memory contention of the
+        // gathers; profiles/r02_d1_chain_floor.txt).  Bit-identical (the tail completes each
+        // tile's sequential sum).  Single rank only; NUFI_D1_SPLIT=0 turns it off.
+        P.split_helpers = 0;
+        if (h->mg_world <= 1 && h->vt_rows >= 4 && !P.two_level && !(getenv("NUFI_D1_SPLIT") && atoi(getenv("NUFI_D1_SPLIT")) == 0)) {
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+            const int helpers = (P.tiles + h->vt_rows - 2) / (h->vt_rows - 1);
+            if (P.tiles + helpers <= sms) {
+                if (!h->row_last) CU(dalloc(&h->row_last, 2 * (size_t)P.tiles * 34 * sizeof(double), h->stream));
+                P.split_helpers = helpers;
+                P.row_last = h->row_last;
+                P.row_last_mm = h->row_last + 2 * (size_t)P.tiles * 32;
+            }
+        }
         if (h->mg_world > 1) {
             if (!h->mg_emulated)
                 for (int q = 0; q < h->mg_world; ++q)

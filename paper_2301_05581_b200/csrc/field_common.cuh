@@ -46,6 +46,11 @@ struct FieldParams {
     int rows_per_block;
     const double *minmax;
     int mm_per_block;
+    // d = 1 split run (run_1d.cu): the last row of every tile is traced by helper CTAs; a tile
+    // row partial is then sums + sums_last (the tile's sequential sum's last add), and the
+    // (min, max) pairs of minmax_last join those of minmax.  Nullable.
+    const double *sums_last;
+    const double *minmax_last;
     const double *rho_in;  // alternative input: a neutral rho (nufi_field_update)
     // step slot
     int64_t slot;
@@ -110,6 +115,10 @@ struct Run1DParams {
     // per-rank local buffers in emulated mode (real mode: tp.partial / tp.fminmax / barrier)
     double *mg_partial[NUFI_MG_MAX], *mg_fminmax[NUFI_MG_MAX];
     unsigned *mg_barrier[NUFI_MG_MAX];
+    // ---- split: helper CTAs trace every tile's last row (single rank, one tile per CTA) ----
+    int split_helpers;     // helper CTAs after the tiles' CTAs (0: no split)
+    double *row_last;      // 2 x (v-tiles x nodes): the last rows, by step parity
+    double *row_last_mm;   // 2 x (tiles x 2): their (min, max) pairs
 };
 
 #define NUFI_STAMP(p, k)                                                              \
@@ -642,12 +651,21 @@ static __device__ __forceinline__ bool field_update_1d_body(const FieldParams &p
     // from there.  The register-load path below is limited by the compiler interleaving
     // each load with its add (one L2 round trip per row).
     const int64_t nsum = (int64_t)B * rpb * N;
-    const bool stage = p.sums && rpb > 1 && p.stage_cap >= nsum + 2 * (int64_t)nmm &&
-                       ((reinterpret_cast<uintptr_t>(p.sums) | reinterpret_cast<uintptr_t>(p.minmax)) & 15) == 0;
+    const bool split = p.sums && p.sums_last;  // tile row partial = sums + sums_last
+    const int64_t nstage = (nsum + 2 * (int64_t)nmm) * (split ? 2 : 1);
+    const bool stage = p.sums && rpb > 1 && p.stage_cap >= nstage &&
+                       ((reinterpret_cast<uintptr_t>(p.sums) | reinterpret_cast<uintptr_t>(p.minmax) |
+                         reinterpret_cast<uintptr_t>(p.sums_last) | reinterpret_cast<uintptr_t>(p.minmax_last)) &
+                        15) == 0;
     double *stg = sm + field_smem_doubles(N, N, true);  // even offset: 16-byte aligned
+    double *stg_last = stg + nsum + 2 * (int64_t)nmm;   // split: the last rows and their pairs
     if (stage) {
         for (int64_t q = t0; q < nsum / 2; q += T) cp_async16(stg + 2 * q, p.sums + 2 * q);
         for (int q = t0; q < nmm; q += T) cp_async16(stg + nsum + 2 * q, p.minmax + 2 * q);
+        if (split) {
+            for (int64_t q = t0; q < nsum / 2; q += T) cp_async16(stg_last + 2 * q, p.sums_last + 2 * q);
+            for (int q = t0; q < nmm; q += T) cp_async16(stg_last + nsum + 2 * q, p.minmax_last + 2 * q);
+        }
         cp_async_wait_all();
         __syncthreads();
         // rows in order per output; rows in chunks of 8 with every load of a chunk issued
@@ -656,26 +674,35 @@ static __device__ __forceinline__ bool field_update_1d_body(const FieldParams &p
         const int logN = 31 - __clz(N), BN = B * N;
         for (int it = t0; it < BN; it += 2 * T) {
             const int it2 = it + T < BN ? it + T : it;
-            const double *s1 = stg + (size_t)(it >> logN) * rpb * N + (it & (N - 1));
-            const double *s2 = stg + (size_t)(it2 >> logN) * rpb * N + (it2 & (N - 1));
+            const size_t o1 = (size_t)(it >> logN) * rpb * N + (it & (N - 1));
+            const size_t o2 = (size_t)(it2 >> logN) * rpb * N + (it2 & (N - 1));
+            const double *s1 = stg + o1, *s2 = stg + o2;
             double S1 = 0.0, S2 = 0.0;
-            int q = 0;
-            for (; q + 8 <= rpb; q += 8) {
-                double a[8], b[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    a[u] = s1[(size_t)(q + u) * N];
-                    b[u] = s2[(size_t)(q + u) * N];
+            if (split) {  // each tile row partial is its sequential sum's last add: s + last
+                const double *l1 = stg_last + o1, *l2 = stg_last + o2;
+                for (int q = 0; q < rpb; ++q) {
+                    S1 += s1[(size_t)q * N] + l1[(size_t)q * N];
+                    S2 += s2[(size_t)q * N] + l2[(size_t)q * N];
                 }
+            } else {
+                int q = 0;
+                for (; q + 8 <= rpb; q += 8) {
+                    double a[8], b[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    S1 += a[u];
-                    S2 += b[u];
+                    for (int u = 0; u < 8; ++u) {
+                        a[u] = s1[(size_t)(q + u) * N];
+                        b[u] = s2[(size_t)(q + u) * N];
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        S1 += a[u];
+                        S2 += b[u];
+                    }
                 }
-            }
-            for (; q < rpb; ++q) {
-                S1 += s1[(size_t)q * N];
-                S2 += s2[(size_t)q * N];
+                for (; q < rpb; ++q) {
+                    S1 += s1[(size_t)q * N];
+                    S2 += s2[(size_t)q * N];
+                }
             }
             sb[it] = S1;
             if (it + T < BN) sb[it + T] = S2;
@@ -683,14 +710,31 @@ static __device__ __forceinline__ bool field_update_1d_body(const FieldParams &p
         for (int q = t0; q < nmm; q += T) {
             mn = fmin(mn, stg[nsum + 2 * q]);
             mx = fmax(mx, stg[nsum + 2 * q + 1]);
+            if (split) {
+                mn = fmin(mn, stg_last[nsum + 2 * q]);
+                mx = fmax(mx, stg_last[nsum + 2 * q + 1]);
+            }
         }
     } else if (t0 < nmm) {
         mn = __ldcg(p.minmax + 2 * t0);
         mx = __ldcg(p.minmax + 2 * t0 + 1);
+        if (split) {
+            mn = fmin(mn, __ldcg(p.minmax_last + 2 * t0));
+            mx = fmax(mx, __ldcg(p.minmax_last + 2 * t0 + 1));
+        }
     }
     // ---- block sums over the block's rows in order (reduce_blocks_kernel order) ----
     if (p.sums && !stage) {
-        if (rpb <= 8) {
+        if (split) {  // each tile row partial is its sequential sum's last add: s + last
+            for (int it = threadIdx.x; it < B * N; it += T) {
+                const int b = it / N, i = it - b * N;
+                const size_t o = (size_t)b * rpb * N + i;
+                double Sb = 0.0;
+                for (int q = 0; q < rpb; ++q)
+                    Sb += __ldcg(p.sums + o + (size_t)q * N) + __ldcg(p.sums_last + o + (size_t)q * N);
+                sb[it] = Sb;
+            }
+        } else if (rpb <= 8) {
             // two outputs per thread per pass: all 2 * rpb loads in flight at once
             for (int it = threadIdx.x; it < B * N; it += 2 * T) {
                 const int it2 = it + T;
@@ -732,6 +776,10 @@ static __device__ __forceinline__ bool field_update_1d_body(const FieldParams &p
         for (int q = t0 + T; q < nmm; q += T) {
             mn = fmin(mn, __ldcg(p.minmax + 2 * q));
             mx = fmax(mx, __ldcg(p.minmax + 2 * q + 1));
+            if (split) {
+                mn = fmin(mn, __ldcg(p.minmax_last + 2 * q));
+                mx = fmax(mx, __ldcg(p.minmax_last + 2 * q + 1));
+            }
         }
     }
     if (p.sums) {

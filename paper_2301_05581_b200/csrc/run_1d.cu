@@ -41,7 +41,7 @@ __host__ __device__ inline size_t run_1d_ring_doubles(int stages, int sps, int s
 // WIDE: 16 tracing warps + producer in one CTA per SM (experiment knob NUFI_D1_WARPS=16)
 // N = 32, 64 run one CTA per SM (the 2 x 64-slab ring fills the SM's shared memory), so their
 // register budget is not halved for a second resident CTA
-template <int NX, int SPS, int WIDE = 0>
+template <int NX, int SPS, int WIDE = 0, int SPLIT = 0>
 __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 32) ? 1 : 2)
     run_1d_kernel(const Run1DParams P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -66,6 +66,12 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 3
     double *const my_fminmax = emu ? P.mg_fminmax[rk] : p.fminmax;
     unsigned *const my_barrier = emu ? P.mg_barrier[rk] : P.barrier;
     const int tiles_r = P.tiles / G, tile_lo = rk * tiles_r;
+    // split (single rank, one tile per CTA, P.split_helpers > 0): owners trace rows 0 .. cw-2 of
+    // their tile, CTAs tiles .. tiles + helpers - 1 trace every tile's last row (<= cw - 1 rows
+    // each), so no SM holds more than cw - 1 tracing warps; the tail completes each tile's
+    // sequential sum with + last row (the same operations, so bit-identical to no split)
+    const bool split = SPLIT && P.split_helpers > 0 && !mg;  // compile-time off for other kernels
+    const bool helper = split && lc >= tiles_r;
 
     // shared memory: [ring | tail workspace (aliased)] | barriers | red | local slab.
     // The tail runs between grid barriers when no bulk copy is in flight (every copy
@@ -111,6 +117,8 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 3
         // step n may write step n+1's partials while a slower one still reads step n's
         double *part = my_partial + (size_t)(n & 1) * P.tiles * 32;
         double *fmm = my_fminmax + (size_t)(n & 1) * P.tiles * 2;
+        double *row_last = split ? P.row_last + (size_t)(n & 1) * P.tiles * 32 : nullptr;
+        double *row_last_mm = split ? P.row_last_mm + (size_t)(n & 1) * P.tiles * 2 : nullptr;
         const int top_cnt = m - (groups - 1) * SPS;
 
         const bool pref_now = pref_ready;
@@ -121,15 +129,20 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 3
         // two independent chains.  Each point's arithmetic and each tile's fixed-order CTA
         // v-sum are unchanged, so the results are bit-identical to one tile per pass.
         constexpr bool PAIR = WIDE != 0;
-        for (int t_loc = lc; t_loc < tiles_r; t_loc += (PAIR ? 2 : 1) * nct) {
+        // (a helper makes exactly one pass: t_loc = lc >= tiles_r)
+        for (int t_loc = lc; t_loc < tiles_r || (helper && t_loc == lc); t_loc += (PAIR ? 2 : 1) * nct) {
             const bool first_tile = t_loc == lc;
-            const bool hasB = PAIR && t_loc + nct < tiles_r;
+            const bool hasB = PAIR && !helper && t_loc + nct < tiles_r;
             static constexpr bool kAlt = false;  // tile mapping: v-tile-major (true) or node-tile-major
             const int vts = P.tiles / p.node_tiles;
+            // a helper's warp w traces the last row of item lc - tiles + w * helpers (split)
+            const int item = helper ? (lc - tiles_r) + warp * P.split_helpers : 0;
+            const bool tracing = helper ? (warp < cw - 1 && item < tiles_r) : (!split || warp < cw - 1);
+            const int row = helper ? cw - 1 : warp;
             int nt2[2], vt2[2], node2[2];
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
-                const int tile = tile_lo + t_loc + (u ? nct : 0);
+                const int tile = tile_lo + (helper ? (item < tiles_r ? item : 0) : t_loc + (u ? nct : 0));
                 nt2[u] = kAlt ? tile / vts : tile % p.node_tiles;
                 vt2[u] = kAlt ? tile % vts : tile / p.node_tiles;
                 node2[u] = nt2[u] * 32 + lane;
@@ -162,14 +175,14 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 3
                 double X2[2], V2[2], v02[2];
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
-                    valid2[u] = node2[u] < nodes && (u == 0 || hasB);
-                    const int j = d1_row(vt2[u], warp, p.vt_per_block, p.B);
+                    valid2[u] = tracing && node2[u] < nodes && (u == 0 || hasB);
+                    const int j = d1_row(vt2[u], row, p.vt_per_block, p.B);
                     v02[u] = __dadd_rn(-p.vmax, __dmul_rn((double)j + 0.5, p.hv));  // grids.py:110-115
                     V2[u] = v02[u] * p.vel_to_scaled;
                     // shifted state (d1_locate), first drift folded
                     X2[u] = ((double)(node2[u] < nodes ? node2[u] : 0) - D1_OFF) - V2[u];
                 }
-                if (n >= 1) {
+                if (n >= 1 && tracing) {
 #pragma unroll
                     for (int u = 0; u < (PAIR ? 2 : 1); ++u) {
                         if (u == 1 && !hasB) break;
@@ -185,7 +198,9 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 3
                     mbar_wait(&full[s_ring], ph_ring);
                     wait_cyc += clock64() - tw0;
                     const double *buf = ring + (size_t)s_ring * SPS * SLAB;
-                    if (NX != 0 && (it > 0 || top_cnt == SPS)) {
+                    if (!tracing) {
+                        // split: a warp without a row keeps the ring protocol only
+                    } else if (NX != 0 && (it > 0 || top_cnt == SPS)) {
                         const unsigned b32 = (unsigned)__cvta_generic_to_shared(buf);
                         if (PAIR && hasB) {
 #pragma unroll
@@ -233,9 +248,31 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 3
                     f2[u] = eval_f0<1>(p.f0, &x, &v);
                 }
             }
+            if (helper) {
+                // split: each tracing warp's row goes to the last-row table as is (the tile's
+                // sequential sum ends with + this row; the tail adds it), its (min, max) alongside
+                if (tracing) {
+                    const double f = f2[0];
+                    if (node2[0] < nodes) row_last[(size_t)vt2[0] * nodes + node2[0]] = valid2[0] ? f : 0.0;
+                    double mn = valid2[0] ? f : DBL_MAX, mx = valid2[0] ? f : -DBL_MAX;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                    }
+                    if (lane == 0) {
+                        const size_t c = (size_t)vt2[0] * p.node_tiles + nt2[0];
+                        row_last_mm[2 * c] = mn;
+                        row_last_mm[2 * c + 1] = mx;
+                    }
+                }
+                continue;
+            }
             // per tile: the fixed-order CTA v-sum in warp 0 (on the critical path to the
-            // barrier), the sampled (min, max) in another warp alongside
+            // barrier), the sampled (min, max) in another warp alongside (split: over the
+            // rows this CTA traced -- the tail adds the last row)
             const int mmw = cw > 1 ? 1 : 0;
+            const int tr = split ? cw - 1 : cw;
 #pragma unroll
             for (int u = 0; u < (PAIR ? 2 : 1); ++u) {
                 if (u == 1 && !hasB) break;
@@ -248,12 +285,12 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 3
                 __syncthreads();
                 if (warp == 0) {
                     double sum = 0.0;
-                    for (int w = 0; w < cw; ++w) sum += red[w * 32 + lane];
+                    for (int w = 0; w < tr; ++w) sum += red[w * 32 + lane];
                     if (node2[u] < nodes) part[(size_t)vt2[u] * nodes + node2[u]] = sum;
                 }
                 if (warp == mmw) {
                     double mn = DBL_MAX, mx = -DBL_MAX;
-                    for (int w = 0; w < cw; ++w) {
+                    for (int w = 0; w < tr; ++w) {
                         mn = fmin(mn, red[32 * cw + w * 32 + lane]);
                         mx = fmax(mx, red[64 * cw + w * 32 + lane]);
                     }
@@ -273,10 +310,10 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 3
         }
 
         {
-            const int my_passes = WIDE ? (my_tiles + 1) / 2 : my_tiles;  // ring streams this step
+            const int my_passes = helper ? 1 : (WIDE ? (my_tiles + 1) / 2 : my_tiles);  // ring streams this step
             gs_mod = (gs_mod + (unsigned)(my_passes * groups) % (unsigned)stages) % (unsigned)stages;
         }
-        pref_ready = P.prefetch && my_tiles > 0 && n < P.n_last && n >= 1;  // (groups_next > 0 iff n >= 1)
+        pref_ready = P.prefetch && (my_tiles > 0 || helper) && n < P.n_last && n >= 1;  // (groups_next > 0 iff n >= 1)
         // all partials of step n are written
         if (P.stamps && blockIdx.x == 0 && threadIdx.x == 0) P.stamps[3 * (n - P.n_first)] = globaltimer();
         if (P.stamps && threadIdx.x == 0 && (n % 400) == 0 && n > 0 && n / 400 <= 4 && blockIdx.x < 1024) {
@@ -296,6 +333,8 @@ __global__ void __launch_bounds__(WIDE ? 544 : 288, (WIDE || NX == 64 || NX == 3
         FieldParams fp = P.fp;
         fp.sums = part;
         fp.minmax = fmm;
+        fp.sums_last = row_last;
+        fp.minmax_last = row_last_mm;
         if (mg) {
             // ---- fused exchange over peer memory: this rank's block sums (the canonical
             // sequential order over the block's tile rows) and block (min, max) are stored
@@ -501,9 +540,9 @@ size_t run_1d_smem_bytes(const TraceRhoParams &p, int threads) {
            2 * p.stages * sizeof(uint64_t) + (3 * 32 * (size_t)cw + p.ev_slab_elems) * sizeof(double);
 }
 
-template <int NX, int SPS, int WIDE = 0>
+template <int NX, int SPS, int WIDE = 0, int SPLIT = 0>
 static cudaError_t launch_run(const Run1DParams &P, int threads, int device, cudaStream_t st, int *grid_out) {
-    auto kern = run_1d_kernel<NX, SPS, WIDE>;
+    auto kern = run_1d_kernel<NX, SPS, WIDE, SPLIT>;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     const int G = P.mg_ranks > 1 ? P.mg_ranks : 1;
@@ -528,6 +567,7 @@ static cudaError_t launch_run(const Run1DParams &P, int threads, int device, cud
         grid = G * args.mg_ctas;
     } else {
         grid = std::min(tiles_launch, per_sm * sms);
+        if (SPLIT) grid = tiles_launch + args.split_helpers;  // helpers after the tiles' CTAs (checked by the caller)
         args.mg_ctas = grid;
     }
     if (grid_out) *grid_out = grid;
@@ -535,12 +575,24 @@ static cudaError_t launch_run(const Run1DParams &P, int threads, int device, cud
     return cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(threads), kargs, smem, st);
 }
 
-cudaError_t launch_run_1d(const Run1DParams &P, int threads, int device, cudaStream_t st, int *grid_out) {
+cudaError_t launch_run_1d(const Run1DParams &P_in, int threads, int device, cudaStream_t st, int *grid_out) {
+    // the split (helper CTAs) exists for the N = 64, 2 x 64-slab kernel only (ts1)
+    Run1DParams P = P_in;
+    if (!(P.tp.N == 64 && P.tp.slabs_per_stage == 64)) P.split_helpers = 0;
     switch (P.tp.N) {
         case 32: return launch_run<32, 16>(P, threads, device, st, grid_out);
         case 64:
             if (P.tp.slabs_per_stage == 32) return launch_run<64, 32>(P, threads, device, st, grid_out);
-            if (P.tp.slabs_per_stage == 64) return launch_run<64, 64>(P, threads, device, st, grid_out);
+            if (P.tp.slabs_per_stage == 64) {
+                // split only when every CTA (tiles + helpers, one per SM) can be co-resident
+                int sms = 0;
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+                if (P.split_helpers > 0 && P.mg_ranks <= 1 && P.tiles + P.split_helpers <= sms)
+                    return launch_run<64, 64, 0, 1>(P, threads, device, st, grid_out);
+                Run1DParams q = P;
+                q.split_helpers = 0;
+                return launch_run<64, 64>(q, threads, device, st, grid_out);
+            }
             return launch_run<64, 16>(P, threads, device, st, grid_out);
         case 128: return launch_run<128, 8>(P, threads, device, st, grid_out);
         case 256:
